@@ -1,0 +1,59 @@
+"""1D building blocks of the oracle (TEST INFRASTRUCTURE ONLY, see oracle/__init__.py).
+
+PAPER.md:599-604 (Appendix A): the 1D shape functions phi_nu of Q_k are the
+Lagrange polynomials on the k+1 Gauss-Lobatto points xi_mu of [0,1],
+phi_nu(xi_mu) = delta_{mu nu}.  Quadrature is exact Gauss-Legendre (reading A3
+of DESIGN.md: the paper names GLL points as *nodes* only; integrals are exact).
+"""
+import numpy as np
+from numpy.polynomial import legendre as npleg
+
+
+def gll_nodes(n):
+    """The n Gauss-Lobatto points on [0,1]: 0, 1 and the n-2 roots
+    of P'_{n-1} mapped from [-1,1].  SPEC.md:125 worked example n=4:
+    {0, (1-1/sqrt5)/2, (1+1/sqrt5)/2, 1}."""
+    if n < 2:
+        raise ValueError("gll_nodes needs n >= 2")
+    m = n - 1                                   # polynomial degree k
+    cm = np.zeros(m + 1)
+    cm[m] = 1.0                                 # P_m in Legendre coefficients
+    inner = np.sort(npleg.legroots(npleg.legder(cm))) if m >= 2 else np.array([])
+    x = np.concatenate([[-1.0], np.real(inner), [1.0]])
+    return (x + 1.0) / 2.0
+
+
+def gauss(n):
+    """n-point Gauss-Legendre rule on [0,1] (library primitive leggauss, mapped).
+    SPEC.md:133 worked example n=2: points (1-+1/sqrt3)/2, weights 1/2."""
+    x, w = npleg.leggauss(n)
+    return (x + 1.0) / 2.0, w / 2.0
+
+
+def lagrange(nodes, x):
+    """Values V[q, j] = phi_j(x_q) and derivatives D[q, j] = phi_j'(x_q) of the
+    Lagrange basis on ``nodes``, by the product formula
+    phi_j(x) = prod_{m != j} (x - xi_m) / (xi_j - xi_m) and its product-rule
+    derivative.  Pure definition, O(n^3) per point."""
+    nodes = np.asarray(nodes, dtype=np.float64)
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    n = len(nodes)
+    V = np.ones((len(x), n))
+    D = np.zeros((len(x), n))
+    for j in range(n):
+        others = [m for m in range(n) if m != j]
+        denom = np.prod([nodes[j] - nodes[m] for m in others])
+        for q, xq in enumerate(x):
+            V[q, j] = np.prod([xq - nodes[m] for m in others]) / denom
+            s = 0.0
+            for a in others:
+                s += np.prod([xq - nodes[m] for m in others if m != a])
+            D[q, j] = s / denom
+    return V, D
+
+
+def penalty(k, h_minus, h_plus, scale=1.0):
+    """gamma_e = k(k+1)(1/h+ + 1/h-).  On a boundary face both
+    sides take the cell's own h (reading A2).  SPEC.md:159 worked
+    example: k=2, h=1/4 -> 48."""
+    return scale * k * (k + 1) * (1.0 / h_plus + 1.0 / h_minus)
