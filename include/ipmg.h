@@ -1,0 +1,178 @@
+/*
+ * ipmg.h -- C ABI of the B200-native multilevel interior-penalty solver
+ * (hot path of arXiv 2405.18982, Cui & Kanschat, "Multilevel Interior Penalty
+ * Methods on GPUs").  Cites refer to /root/reference/PAPER.md line numbers.
+ *
+ * Problem: -Delta u = f on a Cartesian box of cubic cells,
+ * u = 0 on the boundary, symmetric interior penalty DG with Q_k elements on
+ * Gauss-Lobatto nodes, Ax = b.
+ *
+ * Conventions for every call below
+ * --------------------------------
+ *  - Returns ipmg_status; IPMG_OK = 0.  No exception crosses the ABI.  On any
+ *    error a one-line diagnostic is available from ipmg_last_error().
+ *  - Vector arguments are caller-owned, contiguous DEVICE pointers (e.g.
+ *    torch tensors' data_ptr()) of the given precision (double for IPMG_FP64,
+ *    float for IPMG_FP32) and exactly ipmg_level_info() ndofs elements of the level
+ *    named, unless a call says "host".  NULL where a vector is required ->
+ *    IPMG_ERR_INVALID_ARG.  Input and output vectors must not alias unless
+ *    stated.
+ *  - Vector layout ("library order"): on a level
+ *    l >= 1 (all cell counts even) the dofs are grouped by parent cell:
+ *      dof = ((parent_lex * 2^d + child_lex) * (k+1)^d + node_lex)
+ *    parent_lex: lexicographic (x fastest) over the level-(l-1) cells,
+ *    child_lex: x fastest over the 2^d children, node_lex: x fastest over the
+ *    (k+1)^d Gauss-Lobatto nodes of the cell.  Level 0 is cell-wise
+ *    lexicographic (Fig. 5 right).  ipmg_to_cellwise /
+ *    ipmg_from_cellwise convert to/from plain cell-wise lexicographic order.
+ *  - Work is enqueued on cfg.cuda_stream (NULL = legacy default stream) and
+ *    calls return without synchronising, except ipmg_cg_solve (it reads the
+ *    residual norm every iteration) and the host-only utilities.
+ *  - A handle must not be used by two host threads at once.
+ */
+#ifndef IPMG_H
+#define IPMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IPMG_OK = 0,
+  IPMG_ERR_INVALID_ARG = 1,
+  IPMG_ERR_UNSUPPORTED = 2,
+  IPMG_ERR_SIZE_MISMATCH = 3,
+  IPMG_ERR_OUT_OF_MEMORY = 4,
+  IPMG_ERR_CUDA = 5,
+  IPMG_ERR_NCCL = 6,
+  IPMG_ERR_NOT_CONVERGED = 7
+} ipmg_status;
+
+typedef enum { IPMG_FP64 = 0, IPMG_FP32 = 1 } ipmg_precision;
+
+/* Local solver of the vertex-patch smoother ("full" kernel). */
+typedef enum { IPMG_KERNEL_FULL = 0 } ipmg_kernel;
+
+/* Multiplicative = Algorithm 1; additive = BASELINE.json
+ * configs[4] (damped, omega default 1/2^d, reading A17). */
+typedef enum { IPMG_MULTIPLICATIVE = 0, IPMG_ADDITIVE = 1 } ipmg_smoother;
+
+typedef struct {
+  int dim;                  /* 2 or 3 (else IPMG_ERR_INVALID_ARG)                         */
+  int degree;               /* k = 1..7 (else IPMG_ERR_UNSUPPORTED)                       */
+  int coarse_cells[3];      /* T_0 cells per direction, each 1 or 2; default 2 */
+  int n_levels;             /* levels 0..n_levels-1, finest has coarse_cells*2^(n_levels-1)  */
+  double h0;                /* T_0 cell size; unit cube with 2^d coarse cells -> 0.5       */
+  int kernel;               /* ipmg_kernel                                                 */
+  int smoother;             /* ipmg_smoother                                               */
+  double additive_omega;    /* additive damping; <= 0 -> 1/2^d                            */
+  int post_smooth_reverse;  /* 1: post-smoothing visits colours in reverse (symmetric V) */
+  int vcycle_precision;     /* ipmg_precision of the V-cycle; FP32 = PAPER.md:465 mixed  */
+  double penalty_scale;     /* gamma = penalty_scale * k(k+1)(1/h+ + 1/h-); default 1     */
+  int device;               /* CUDA device ordinal                                         */
+  void *cuda_stream;        /* cudaStream_t all work is enqueued on                        */
+} ipmg_config;
+
+typedef struct ipmg_handle ipmg_handle;
+
+typedef struct {
+  int iterations;           /* n = number of A-applications until ||r_n|| <= rtol ||r_0|| */
+  double nu;                /* fractional iteration count -8 n / log10(||r_n||/||r_0||) (reading A6) */
+  double rel_residual;      /* ||r_n|| / ||r_0||                                           */
+  double seconds;           /* host wall time of the solve (setup excluded)                */
+  int history_len;          /* entries written to history                                  */
+  double *history;          /* HOST, caller-owned, capacity history_cap: ||r_0||..||r_n|| */
+  int history_cap;
+} ipmg_solve_info;
+
+/* Fill *cfg with defaults: dim 3, degree 4, coarse 2x2x2, 3 levels, h0 0.5, full
+ * kernel, multiplicative, reverse post-smoothing, FP32 V-cycle, penalty 1. */
+void ipmg_config_default(ipmg_config *cfg);
+
+/* Host setup + device workspace (PAPER.md:142-147 hierarchy, 259-280 1D
+ * eigenpairs).  *out is library-owned; free with ipmg_destroy.  Errors:
+ * INVALID_ARG (dim, n_levels < 1, coarse_cells not in {1,2}, h0 <= 0),
+ * UNSUPPORTED (degree), OUT_OF_MEMORY, CUDA. */
+ipmg_status ipmg_create(const ipmg_config *cfg, ipmg_handle **out);
+ipmg_status ipmg_destroy(ipmg_handle *h);
+
+/* Level geometry.  ndofs = cells * (k+1)^d; cells[3] (cells[2] = 1 in 2D); hsize = h0/2^l. */
+ipmg_status ipmg_level_info(const ipmg_handle *h, int level, int64_t *ndofs, int cells[3],
+                            double *hsize);
+
+/* y = A_l x, the SIPG operator on level l applied matrix-free, patch-wise over
+ * the colour-0 vertex patches (Fig. 1).  x, y: level l. */
+ipmg_status ipmg_vmult(ipmg_handle *h, int level, int precision, const void *x, void *y);
+
+/* One smoothing step x <- S_l(x, b) on level l >= 1, in place.  Multiplicative:
+ * Algorithm 1 with the full kernel, residual from the
+ * pre-colour state, colours 0..2^d-1 (reverse != 0: reversed).
+ * Additive: x <- x + omega sum_j R_j^T A_j^{-1} R_j (b - A x). */
+ipmg_status ipmg_smooth(ipmg_handle *h, int level, int precision, void *x, const void *b,
+                        int reverse);
+
+/* One colour of Algorithm 1: x_out = x_in + sum_{j in colour} R_j^T A_j^{-1} R_j (b - A x_in)
+ * (patches of the colour solved exactly; cells not covered by the colour are
+ * copied).  x_in may be NULL (= zero vector).  x_out must not alias x_in. */
+ipmg_status ipmg_smooth_colour(ipmg_handle *h, int level, int precision, const void *x_in,
+                               const void *b, void *x_out, int colour);
+
+/* r_c = P^T (b - A_l x) on level l >= 1 into level l-1 (restriction =
+ * transpose of the canonical embedding, reading A4).  x may be NULL (= 0), giving
+ * r_c = P^T b. */
+ipmg_status ipmg_residual_restrict(ipmg_handle *h, int fine_level, int precision, const void *x,
+                                   const void *b, void *r_c);
+
+/* x_f += P e_c: canonical embedding from level fine_level-1. */
+ipmg_status ipmg_prolongate_add(ipmg_handle *h, int fine_level, int precision, const void *e_c,
+                                void *x_f);
+
+/* x0 = A_0^{-1} b0 on level 0 by global fast diagonalisation (
+ * eq. inverse2d/3d with global 1D eigenpairs, reading A10). */
+ipmg_status ipmg_coarse_solve(ipmg_handle *h, int precision, const void *b0, void *x0);
+
+/* z = P_L^{-1} r: one V-cycle on the finest level, in
+ * cfg.vcycle_precision (converted on entry/exit).  r, z: double,
+ * finest level, may not alias. */
+ipmg_status ipmg_vcycle(ipmg_handle *h, const double *r, double *z);
+
+/* GMG-preconditioned CG on the finest level (north star; PAPER.md:331 stopping
+ * rule ||r_n||_2 <= rtol ||r_0||_2, x_0 = 0).  b, x: double device vectors;
+ * info may be NULL.  Returns IPMG_ERR_NOT_CONVERGED (info still filled) when
+ * max_it is reached; b = 0 returns OK with 0 iterations. */
+ipmg_status ipmg_cg_solve(ipmg_handle *h, const double *b, double *x, double rtol, int max_it,
+                          ipmg_solve_info *info);
+
+/* Right-hand side b_i = int f phi_i on level `level` for f == 1;
+ * kind must be 0.  b: double device vector of that level. */
+ipmg_status ipmg_rhs(ipmg_handle *h, int level, int kind, double *b);
+
+/* Layout conversion library order <-> cell-wise lexicographic order. */
+ipmg_status ipmg_to_cellwise(ipmg_handle *h, int level, int precision, const void *x_lib,
+                             void *x_cellwise);
+ipmg_status ipmg_from_cellwise(ipmg_handle *h, int level, int precision, const void *x_cellwise,
+                               void *x_lib);
+
+/* Synchronise the handle's stream; returns IPMG_ERR_CUDA on an asynchronous fault. */
+ipmg_status ipmg_synchronize(ipmg_handle *h);
+
+/* One-line diagnostic of the last error on h (or of the last failed create
+ * when h is NULL).  Library-owned string. */
+const char *ipmg_last_error(const ipmg_handle *h);
+
+/* HOST-ONLY utility (no GPU needed): the unit-h 1D tables of degree k the
+ * kernels use, for inspection/tests.  `what`: 0 nodes (k+1), 1 mass (k+1)^2,
+ * 2 stiffness (k+1)^2, 3+v patch matrix L^P_v (2k+2)^2 for variant v in 0..3
+ * (bit0: low face on boundary, bit1: high face on boundary), 7+v patch
+ * eigenvectors S_v (row-major, column m = mode m), 11+v eigenvalues (2k+2),
+ * 15 prolongation (2k+2)x(k+1).  Writes at most cap doubles to out (host);
+ * *len = number of entries.  Errors: UNSUPPORTED (k), INVALID_ARG. */
+ipmg_status ipmg_tables_1d(int k, double penalty_scale, int what, double *out, int cap, int *len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IPMG_H */

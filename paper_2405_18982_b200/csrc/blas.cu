@@ -1,0 +1,270 @@
+// Degree-independent kernels: precision casts, deterministic dot products, the
+// fused PCG vector updates, layout permutation, right-hand side and the coarse
+// fast-diagonalisation solve.
+//
+// Reductions are deterministic: a fixed grid of RED_BLOCKS blocks, each
+// accumulating a fixed strided subset in fp64 and reducing in shared memory
+// with a fixed tree; a single-block finalize sums the partials in order.
+#include "blas.cuh"
+
+namespace ipmg {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  // warp shuffle tree, then one warp over the per-warp sums
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;   // valid in thread 0
+}
+
+template <typename TA, typename TB>
+__global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const TA* __restrict__ a, const TB* __restrict__ b,
+                                                                   long long n, double* __restrict__ partial) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s = fma((double)a[i], (double)b[i], s);
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double* __restrict__ partial, int np,
+                                                                double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += partial[i];
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// x += alpha p ; r -= alpha q ; partial ||r||^2   with alpha = s[i_rz] / s[i_pq]
+__global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                             const double* __restrict__ p, const double* __restrict__ q,
+                                                             long long n, const double* __restrict__ sc, int i_rz,
+                                                             int i_pq, double* __restrict__ partial) {
+  __shared__ double sh[32];
+  const double alpha = sc[i_rz] / sc[i_pq];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// p = z + beta p, beta = s[i_new] / s[i_old]
+__global__ void cg_p_kernel(double* __restrict__ p, const double* __restrict__ z, long long n,
+                            const double* __restrict__ sc, int i_new, int i_old) {
+  const double beta = sc[i_new] / sc[i_old];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+// zd = (double) zf ; partial r . zd
+__global__ void __launch_bounds__(RED_THREADS) cast_dot_kernel(const float* __restrict__ zf, double* __restrict__ zd,
+                                                                const double* __restrict__ r, long long n,
+                                                                double* __restrict__ partial) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double z = (double)zf[i];
+    zd[i] = z;
+    s = fma(r[i], z, s);
+  }
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+template <typename TI, typename TO>
+__global__ void cast_kernel(const TI* __restrict__ in, TO* __restrict__ out, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = (TO)in[i];
+}
+
+// to_cellwise: out[cell_lex*cell + l] = in[lib(cell)*cell + l]; from_cellwise the inverse
+template <typename T, bool TO_CW>
+__global__ void permute_kernel(const T* __restrict__ in, T* __restrict__ out, LevelGeom g, int cell, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / cell;
+    const int l = (int)(e % cell);
+    const int cx = (int)(c % g.n[0]);
+    const int cy = (int)((c / g.n[0]) % g.n[1]);
+    const int cz = (int)(c / ((long long)g.n[0] * g.n[1]));
+    const long long lib = cell_offset_cells(g, cx, cy, cz) * cell + l;
+    if (TO_CW) out[e] = in[lib];
+    else out[lib] = in[e];
+  }
+}
+
+__global__ void pattern_fill_kernel(double* __restrict__ b, const double* __restrict__ pat, int cell, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    b[e] = pat[e % cell];
+}
+
+// Coarse solve x0 = A_0^{-1} b0 by global fast diagonalisation on level 0
+// (lexicographic cells); one CTA, tensor of N0 x N1 (x N2) global nodes in smem.
+template <typename T>
+__global__ void coarse_fd_kernel(const T* __restrict__ b, T* __restrict__ x, CoarseDesc cd, const T* __restrict__ S0,
+                                 const T* __restrict__ S1, const T* __restrict__ S2, const T* __restrict__ l0,
+                                 const T* __restrict__ l1, const T* __restrict__ l2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* X = reinterpret_cast<T*>(smem_raw);
+  const int N0 = cd.N[0], N1 = cd.N[1], N2 = cd.N[2], nc = cd.nc, d = cd.dim;
+  const int total = N0 * N1 * N2;
+  const int cell = (d == 2) ? nc * nc : nc * nc * nc;
+  const T* S[3] = {S0, S1, S2};
+  const T* L[3] = {l0, l1, l2};
+  // load: global node (g0,g1,g2) <- cell (g/nc), node (g%nc)
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int g0 = e % N0, g1 = (e / N0) % N1, g2 = e / (N0 * N1);
+    const int c0 = g0 / nc, c1 = g1 / nc, c2 = g2 / nc;
+    const int loc = (g0 % nc) + nc * ((g1 % nc) + nc * (g2 % nc));
+    const long long off = ((long long)c0 + cd.n0[0] * (c1 + (long long)cd.n0[1] * c2)) * cell + loc;
+    X[e] = (T)cd.scale * b[off];
+  }
+  __syncthreads();
+  const int Ns[3] = {N0, N1, N2};
+  const int strides[3] = {1, N0, N0 * N1};
+  // forward S^T along each direction, divide, S back
+  for (int pass = 0; pass < 2 * d + 1; ++pass) {
+    if (pass == d) {
+      for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int g0 = e % N0, g1 = (e / N0) % N1, g2 = e / (N0 * N1);
+        T ls = L[0][g0] + L[1][g1];
+        if (d == 3) ls += L[2][g2];
+        X[e] = X[e] / ls;
+      }
+      __syncthreads();
+      continue;
+    }
+    const bool fwd = pass < d;
+    const int a = fwd ? pass : (2 * d - pass);
+    const int N = Ns[a], st = strides[a];
+    const int nlines = total / N;
+    for (int li = threadIdx.x; li < nlines; li += blockDim.x) {
+      // base of line li along a
+      int base;
+      if (a == 0) base = li * N0;
+      else if (a == 1) base = (li % N0) + (li / N0) * N0 * N1;
+      else base = li;
+      T v[CoarseDesc::NMAX], w[CoarseDesc::NMAX];
+      for (int j = 0; j < N; ++j) v[j] = X[base + j * st];
+      for (int i = 0; i < N; ++i) {
+        T acc = T(0);
+        for (int j = 0; j < N; ++j) acc += (fwd ? S[a][j * N + i] : S[a][i * N + j]) * v[j];
+        w[i] = acc;
+      }
+      for (int j = 0; j < N; ++j) X[base + j * st] = w[j];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int g0 = e % N0, g1 = (e / N0) % N1, g2 = e / (N0 * N1);
+    const int c0 = g0 / nc, c1 = g1 / nc, c2 = g2 / nc;
+    const int loc = (g0 % nc) + nc * ((g1 % nc) + nc * (g2 % nc));
+    const long long off = ((long long)c0 + cd.n0[0] * (c1 + (long long)cd.n0[1] * c2)) * cell + loc;
+    x[off] = X[e];
+  }
+}
+
+inline int grid_for(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 8 * 148) g = 8 * 148;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+cudaError_t dot_partial(int prec_a, int prec_b, const void* a, const void* b, long long n, double* partial,
+                        cudaStream_t s) {
+  if (prec_a == 0 && prec_b == 0)
+    dot_partial_kernel<double, double><<<RED_BLOCKS, RED_THREADS, 0, s>>>((const double*)a, (const double*)b, n, partial);
+  else if (prec_a == 1 && prec_b == 1)
+    dot_partial_kernel<float, float><<<RED_BLOCKS, RED_THREADS, 0, s>>>((const float*)a, (const float*)b, n, partial);
+  else if (prec_a == 0 && prec_b == 1)
+    dot_partial_kernel<double, float><<<RED_BLOCKS, RED_THREADS, 0, s>>>((const double*)a, (const float*)b, n, partial);
+  else
+    dot_partial_kernel<float, double><<<RED_BLOCKS, RED_THREADS, 0, s>>>((const float*)a, (const double*)b, n, partial);
+  return cudaGetLastError();
+}
+
+cudaError_t finalize(const double* partial, double* out, cudaStream_t s) {
+  finalize_kernel<<<1, RED_THREADS, 0, s>>>(partial, RED_BLOCKS, out);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_update_xr(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
+                         int i_rz, int i_pq, double* partial, cudaStream_t s) {
+  cg_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_update_p(double* p, const double* z, long long n, const double* sc, int i_new, int i_old,
+                        cudaStream_t s) {
+  cg_p_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, z, n, sc, i_new, i_old);
+  return cudaGetLastError();
+}
+
+cudaError_t cast_f2d_dot(const float* zf, double* zd, const double* r, long long n, double* partial, cudaStream_t s) {
+  cast_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(zf, zd, r, n, partial);
+  return cudaGetLastError();
+}
+
+cudaError_t cast(int prec_in, int prec_out, const void* in, void* out, long long n, cudaStream_t s) {
+  if (prec_in == prec_out) return cudaMemcpyAsync(out, in, n * (prec_in == 0 ? 8 : 4), cudaMemcpyDeviceToDevice, s);
+  if (prec_in == 0)
+    cast_kernel<double, float><<<grid_for(n, 256), 256, 0, s>>>((const double*)in, (float*)out, n);
+  else
+    cast_kernel<float, double><<<grid_for(n, 256), 256, 0, s>>>((const float*)in, (double*)out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t permute(int prec, bool to_cellwise, const void* in, void* out, const LevelGeom& g, int cell, long long n,
+                    cudaStream_t s) {
+  const int grid = grid_for(n, 256);
+  if (prec == 0) {
+    if (to_cellwise) permute_kernel<double, true><<<grid, 256, 0, s>>>((const double*)in, (double*)out, g, cell, n);
+    else permute_kernel<double, false><<<grid, 256, 0, s>>>((const double*)in, (double*)out, g, cell, n);
+  } else {
+    if (to_cellwise) permute_kernel<float, true><<<grid, 256, 0, s>>>((const float*)in, (float*)out, g, cell, n);
+    else permute_kernel<float, false><<<grid, 256, 0, s>>>((const float*)in, (float*)out, g, cell, n);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t pattern_fill(double* b, const double* pat, int cell, long long n, cudaStream_t s) {
+  pattern_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(b, pat, cell, n);
+  return cudaGetLastError();
+}
+
+cudaError_t coarse_solve(int prec, const void* b, void* x, const CoarseDesc& cd, const void* const S[3],
+                         const void* const L[3], cudaStream_t s) {
+  const size_t bytes = (size_t)cd.N[0] * cd.N[1] * cd.N[2] * (prec == 0 ? 8 : 4);
+  if (prec == 0) {
+    cudaFuncSetAttribute(coarse_fd_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    coarse_fd_kernel<double><<<1, 256, bytes, s>>>((const double*)b, (double*)x, cd, (const double*)S[0],
+                                                   (const double*)S[1], (const double*)S[2], (const double*)L[0],
+                                                   (const double*)L[1], (const double*)L[2]);
+  } else {
+    cudaFuncSetAttribute(coarse_fd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    coarse_fd_kernel<float><<<1, 256, bytes, s>>>((const float*)b, (float*)x, cd, (const float*)S[0],
+                                                  (const float*)S[1], (const float*)S[2], (const float*)L[0],
+                                                  (const float*)L[1], (const float*)L[2]);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ipmg

@@ -1,0 +1,73 @@
+// Shared device-side definitions of the ipmg kernels (sm_100a).
+//
+// Geometry: a level has n[a] cubic cells per direction (n[2] = 1 in 2D), size
+// h; the operator scales as A_h = h^(d-2) A_1 (mass ~ h, stiffness, penalty and
+// traces ~ 1/h), so every table is a unit-h table and a level only carries the
+// scalar hs = h^(d-2) (PAPER.md:118-126 Kronecker form with h-scaled 1D factors).
+//
+// Layout: cell chunks of (k+1)^d node values
+// (lexicographic, x fastest).  Level l >= 1 groups the 2^d children of each
+// level-(l-1) cell contiguously ("parent-grouped"); level 0 is lexicographic.
+// A colour-0 vertex patch is exactly one parent cell, so its 2^d cells form one
+// contiguous chunk; a shifted colour reads 2^d separate contiguous cell chunks.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ipmg {
+
+struct LevelGeom {
+  int n[3];            // cells per direction
+  int grouped;         // 1: parent-grouped layout, 0: lexicographic cells
+  long long ncells;
+  double hs;           // h^(d-2)
+  double hinv;         // h^(2-d)
+};
+
+__host__ __device__ __forceinline__ long long cell_offset_cells(const LevelGeom& g, int cx, int cy,
+                                                                int cz) {
+  // index of the cell chunk (in units of cells)
+  if (g.grouped) {
+    const int PX = g.n[0] >> 1, PY = g.n[1] >> 1;
+    const int qx = cx & 1, qy = cy & 1, qz = cz & 1;
+    const long long plin = (long long)(cx >> 1) + (long long)PX * ((cy >> 1) + (long long)PY * (cz >> 1));
+    const int nchild = (g.n[2] > 1) ? 8 : 4;   // 2^d (n[2] == 1 only in 2D)
+    return plin * nchild + qx + 2 * qy + 4 * qz;
+  }
+  return (long long)cx + (long long)g.n[0] * (cy + (long long)g.n[1] * cz);
+}
+
+// Device-side 1D tables for degree K in precision T (unit h); one instance per
+// precision lives in __constant__ memory of each per-degree translation unit.
+template <int K, typename T>
+struct TabData {
+  static constexpr int NC = K + 1, NP = 2 * (K + 1);
+  T M[NC][NC];          // cell mass
+  T LP[4][NP][NP];      // 2-cell patch stiffness + face terms, variant v
+  T S[4][NP][NP];       // eigenvectors, S[v][node][mode]
+  T lam[4][NP];         // eigenvalues
+  T d0[NC], d1[NC];     // phi_j'(0), phi_j'(1)
+  T P[NP][NC];          // prolongation (patch-lex fine node, coarse node)
+  T w[NC];              // int phi_i
+  T gamma;              // unit penalty 2k(k+1)*scale
+};
+
+// Per-degree launcher table exported by each kernels_k<K>.cu.
+struct KernelSet {
+  int k;
+  cudaError_t (*upload)(const void* tab64, const void* tab32, size_t bytes64, size_t bytes32);
+  size_t tab_bytes64, tab_bytes32;
+  // all launchers: prec 0 = double, 1 = float; dim 2 or 3
+  cudaError_t (*vmult)(int dim, int prec, const void* x, void* y, const LevelGeom& g,
+                       const void* b_minus, cudaStream_t s);
+  cudaError_t (*smooth)(int dim, int prec, const void* x_in, const void* b, void* x_out,
+                        const LevelGeom& g, int colour, cudaStream_t s);
+  cudaError_t (*additive)(int dim, int prec, const void* r, void* x, const LevelGeom& g, int colour,
+                          double omega, cudaStream_t s);
+  cudaError_t (*restrict_)(int dim, int prec, const void* x, const void* b, void* rc,
+                           const LevelGeom& gf, const LevelGeom& gc, cudaStream_t s);
+  cudaError_t (*prolong)(int dim, int prec, const void* ec, void* xf, const LevelGeom& gf,
+                         const LevelGeom& gc, cudaStream_t s);
+};
+
+}  // namespace ipmg

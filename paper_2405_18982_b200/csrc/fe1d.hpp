@@ -1,0 +1,48 @@
+// Host-side 1D finite-element setup for the ipmg library (layer 1 of the build).
+//
+// Everything the sm_100a kernels need is derived from 1D objects on the unit
+// interval (h = 1); a level of size h scales the whole operator by h^(d-2)
+// (mass ~ h, stiffness/penalty/derivatives ~ 1/h), so the tables are level
+// independent.  Sources:
+//   * GLL Lagrange basis ............ PAPER.md:599-604 (Appendix A)
+//   * SIPG form, penalty ............ PAPER.md:81-100 (eq. jump_mean, bilinear_form)
+//   * Kronecker cell matrices ....... PAPER.md:118-126
+//   * fast diagonalisation .......... PAPER.md:259-280 (eq. inverse2d/3d, fast_inverse)
+//   * canonical-embedding transfer .. PAPER.md:152
+// Independent of oracle/ (different language, algorithms: Newton for the
+// Legendre roots, Kronecker patch matrices, Jacobi eigen-solver).
+#pragma once
+#include <vector>
+
+namespace ipmg {
+
+struct FE1D {
+  int k = 0, nc = 0, np = 0;       // degree, nodes per cell, nodes per 2-cell patch
+  double gamma = 0;                // unit-h penalty 2k(k+1)*scale (reading A2)
+  std::vector<double> nodes;       // GLL nodes on [0,1]                       (nc)
+  std::vector<double> w;           // int_0^1 phi_i                             (nc)
+  std::vector<double> M, K;        // unit cell mass / stiffness, row-major    (nc*nc)
+  std::vector<double> d0, d1;      // phi_j'(0), phi_j'(1)                     (nc)
+  // 2-cell patch matrices, variant v: bit0 = low outer face on the domain
+  // boundary, bit1 = high outer face on the domain boundary.
+  std::vector<double> MP;          // patch mass (block diagonal)             (np*np)
+  std::vector<double> LP[4];       // patch stiffness + face terms            (np*np)
+  std::vector<double> S[4];        // generalized eigenvectors, S[i*np+m] = node i, mode m
+  std::vector<double> lam[4];      // eigenvalues ascending                    (np)
+  std::vector<double> P;           // prolongation, P[i*nc+j] = phi_j((xi_{i%nc} + i/nc)/2)  (np*nc)
+};
+
+// Build all unit tables for degree k (1..7); penalty_scale multiplies gamma.
+FE1D build_fe1d(int k, double penalty_scale);
+
+// Global 1D SIPG matrix (unit h) on ncell cells with boundary faces at both ends
+// and its mass; row-major (ncell*nc)^2.  Used for the coarse solve (reading A10).
+void global_1d(const FE1D& fe, int ncell, std::vector<double>& L, std::vector<double>& M);
+
+// Generalized symmetric eigenproblem L S = M S diag(lam), S^T M S = I, lam ascending,
+// sign fixed so that the largest-|.| entry of each column is positive.
+// Cholesky + cyclic Jacobi.  Returns false if M is not SPD.
+bool gen_eig(int n, const std::vector<double>& L, const std::vector<double>& M,
+             std::vector<double>& S, std::vector<double>& lam);
+
+}  // namespace ipmg

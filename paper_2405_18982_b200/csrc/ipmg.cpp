@@ -1,0 +1,558 @@
+// C ABI of the ipmg library: handle, host setup, V-cycle and PCG drivers.
+// The declarations and their contracts are in include/ipmg.h.
+#include "ipmg.h"
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "blas.cuh"
+#include "common.cuh"
+#include "fe1d.hpp"
+
+ipmg::KernelSet ipmg_kernel_set_k1();
+ipmg::KernelSet ipmg_kernel_set_k2();
+ipmg::KernelSet ipmg_kernel_set_k3();
+ipmg::KernelSet ipmg_kernel_set_k4();
+ipmg::KernelSet ipmg_kernel_set_k5();
+ipmg::KernelSet ipmg_kernel_set_k6();
+ipmg::KernelSet ipmg_kernel_set_k7();
+
+namespace {
+
+std::string g_create_error;
+
+ipmg::KernelSet kernel_set(int k) {
+  switch (k) {
+    case 1: return ipmg_kernel_set_k1();
+    case 2: return ipmg_kernel_set_k2();
+    case 3: return ipmg_kernel_set_k3();
+    case 4: return ipmg_kernel_set_k4();
+    case 5: return ipmg_kernel_set_k5();
+    case 6: return ipmg_kernel_set_k6();
+    default: return ipmg_kernel_set_k7();
+  }
+}
+
+// Host copy of TabData<K,T> laid out exactly like the device struct.
+template <typename T>
+std::vector<unsigned char> pack_tables(const ipmg::FE1D& fe, size_t bytes) {
+  const int nc = fe.nc, np = fe.np;
+  std::vector<T> v;
+  v.reserve(bytes / sizeof(T));
+  for (int i = 0; i < nc * nc; ++i) v.push_back((T)fe.M[i]);
+  for (int var = 0; var < 4; ++var)
+    for (int i = 0; i < np * np; ++i) v.push_back((T)fe.LP[var][i]);
+  for (int var = 0; var < 4; ++var)
+    for (int i = 0; i < np * np; ++i) v.push_back((T)fe.S[var][i]);
+  for (int var = 0; var < 4; ++var)
+    for (int i = 0; i < np; ++i) v.push_back((T)fe.lam[var][i]);
+  for (int i = 0; i < nc; ++i) v.push_back((T)fe.d0[i]);
+  for (int i = 0; i < nc; ++i) v.push_back((T)fe.d1[i]);
+  for (int i = 0; i < np * nc; ++i) v.push_back((T)fe.P[i]);
+  for (int i = 0; i < nc; ++i) v.push_back((T)fe.w[i]);
+  v.push_back((T)fe.gamma);
+  std::vector<unsigned char> out(bytes, 0);
+  const size_t used = v.size() * sizeof(T);
+  if (used <= bytes) std::memcpy(out.data(), v.data(), used);
+  return out;
+}
+
+}  // namespace
+
+struct ipmg_handle {
+  ipmg_config cfg{};
+  int dim = 3, k = 1, nc = 2, cell = 8, nlev = 1;
+  cudaStream_t stream = nullptr;
+  ipmg::KernelSet ks{};
+  ipmg::FE1D fe;
+  std::vector<ipmg::LevelGeom> geom;
+  std::vector<long long> ndofs;
+  std::vector<double> hsize;
+  // V-cycle / API workspace: [prec][level]
+  std::vector<void*> vx0[2], vx1[2], vb[2], scratch[2];
+  // coarse FD tables per precision and direction
+  void* cS[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  void* cL[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  ipmg::CoarseDesc cdesc{};
+  // PCG workspace (finest level, fp64)
+  double *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr;
+  double *partial = nullptr, *scal = nullptr, *hpin = nullptr, *pattern = nullptr;
+  std::vector<void*> allocs;
+  std::string err;
+
+  ipmg_status fail(ipmg_status st, const std::string& msg) {
+    err = msg;
+    return st;
+  }
+  ipmg_status cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return IPMG_OK;
+    err = std::string(what) + ": " + cudaGetErrorString(e);
+    return IPMG_ERR_CUDA;
+  }
+  void* dalloc(size_t bytes) {
+    void* ptr = nullptr;
+    if (cudaMalloc(&ptr, bytes) != cudaSuccess) return nullptr;
+    allocs.push_back(ptr);
+    return ptr;
+  }
+  size_t esize(int prec) const { return prec == IPMG_FP64 ? 8 : 4; }
+  ipmg_status ensure_scratch(int prec, int level) {
+    if (scratch[prec][level]) return IPMG_OK;
+    scratch[prec][level] = dalloc(ndofs[level] * esize(prec));
+    return scratch[prec][level] ? IPMG_OK : fail(IPMG_ERR_OUT_OF_MEMORY, "scratch allocation failed");
+  }
+  ipmg_status ensure_vcycle(int prec) {
+    if (!vx0[prec].empty() && vx0[prec][0]) return IPMG_OK;
+    vx0[prec].assign(nlev, nullptr);
+    vx1[prec].assign(nlev, nullptr);
+    vb[prec].assign(nlev, nullptr);
+    for (int l = 0; l < nlev; ++l) {
+      vx0[prec][l] = dalloc(ndofs[l] * esize(prec));
+      vx1[prec][l] = dalloc(ndofs[l] * esize(prec));
+      vb[prec][l] = dalloc(ndofs[l] * esize(prec));
+      if (!vx0[prec][l] || !vx1[prec][l] || !vb[prec][l])
+        return fail(IPMG_ERR_OUT_OF_MEMORY, "V-cycle workspace allocation failed");
+    }
+    return IPMG_OK;
+  }
+
+  // ------------------------------------------------------------ building blocks
+  ipmg_status smooth_colour(int level, int prec, const void* xi, const void* b, void* xo, int colour) {
+    return cuda(ks.smooth(dim, prec, xi, b, xo, geom[level], colour, stream), "smooth_colour");
+  }
+  // multiplicative step: passes ping-pong between x and other; 2^d passes -> ends in x
+  ipmg_status smooth_mult(int level, int prec, void* x, void* other, const void* b, bool reverse, bool x_is_zero) {
+    const int ncol = 1 << dim;
+    void* cur = x;
+    void* nxt = other;
+    for (int i = 0; i < ncol; ++i) {
+      const int c = reverse ? ncol - 1 - i : i;
+      ipmg_status st = smooth_colour(level, prec, (i == 0 && x_is_zero) ? nullptr : cur, b, nxt, c);
+      if (st != IPMG_OK) return st;
+      std::swap(cur, nxt);
+    }
+    return IPMG_OK;
+  }
+  double omega() const {
+    return cfg.additive_omega > 0 ? cfg.additive_omega : 1.0 / (1 << dim);
+  }
+  // additive step: x += omega sum_j R_j^T A_j^{-1} R_j (b - A x); rbuf: residual scratch
+  ipmg_status smooth_add(int level, int prec, void* x, void* rbuf, const void* b, bool x_is_zero) {
+    const void* r = b;
+    if (!x_is_zero) {
+      ipmg_status st = cuda(ks.vmult(dim, prec, x, rbuf, geom[level], b, stream), "residual");
+      if (st != IPMG_OK) return st;
+      r = rbuf;
+    } else {
+      ipmg_status st = cuda(cudaMemsetAsync(x, 0, ndofs[level] * esize(prec), stream), "memset");
+      if (st != IPMG_OK) return st;
+    }
+    for (int c = 0; c < (1 << dim); ++c) {
+      ipmg_status st = cuda(ks.additive(dim, prec, r, x, geom[level], c, omega(), stream), "additive");
+      if (st != IPMG_OK) return st;
+    }
+    return IPMG_OK;
+  }
+  ipmg_status coarse(int prec, const void* b, void* x) {
+    const void* S[3] = {cS[prec][0], cS[prec][1], cS[prec][2]};
+    const void* L[3] = {cL[prec][0], cL[prec][1], cL[prec][2]};
+    return cuda(ipmg::coarse_solve(prec, b, x, cdesc, S, L, stream), "coarse_solve");
+  }
+  // one V-cycle on level l of the workspace of precision prec: input vb[l],
+  // output vx1[l]
+  ipmg_status vcycle_level(int l, int prec) {
+    void* b = vb[prec][l];
+    void* const x0 = vx0[prec][l];
+    void* const x1 = vx1[prec][l];
+    if (l == 0) return coarse(prec, b, x1);
+    ipmg_status st;
+    const bool additive = cfg.smoother == IPMG_ADDITIVE;
+    // (1) pre-smoothing from x = 0; smooth_* leave the result in their first buffer
+    if (additive) st = smooth_add(l, prec, x1, x0, b, true);
+    else st = smooth_mult(l, prec, x1, x0, b, false, true);
+    if (st != IPMG_OK) return st;
+    // (2) coarse-grid correction x1 += P P_{l-1}^{-1} P^T (b - A x1)
+    st = cuda(ks.restrict_(dim, prec, x1, b, vb[prec][l - 1], geom[l], geom[l - 1], stream), "restrict");
+    if (st != IPMG_OK) return st;
+    st = vcycle_level(l - 1, prec);
+    if (st != IPMG_OK) return st;
+    st = cuda(ks.prolong(dim, prec, vx1[prec][l - 1], x1, geom[l], geom[l - 1], stream), "prolong");
+    if (st != IPMG_OK) return st;
+    // (3) post-smoothing (colours reversed for a symmetric V-cycle, reading A7)
+    if (additive) return smooth_add(l, prec, x1, x0, b, false);
+    return smooth_mult(l, prec, x1, x0, b, cfg.post_smooth_reverse != 0, false);
+  }
+  ipmg_status vcycle(const double* r, double* z, double* rz_partial) {
+    const int prec = cfg.vcycle_precision;
+    const int L = nlev - 1;
+    ipmg_status st = ensure_vcycle(prec);
+    if (st != IPMG_OK) return st;
+    st = cuda(ipmg::cast(0, prec, r, vb[prec][L], ndofs[L], stream), "cast in");
+    if (st != IPMG_OK) return st;
+    st = vcycle_level(L, prec);
+    if (st != IPMG_OK) return st;
+    if (rz_partial && prec == IPMG_FP32)
+      return cuda(ipmg::cast_f2d_dot((const float*)vx1[prec][L], z, r, ndofs[L], rz_partial, stream), "cast out");
+    st = cuda(ipmg::cast(prec, 0, vx1[prec][L], z, ndofs[L], stream), "cast out");
+    if (st != IPMG_OK || !rz_partial) return st;
+    return cuda(ipmg::dot_partial(0, 0, r, z, ndofs[L], rz_partial, stream), "dot");
+  }
+};
+
+extern "C" {
+
+void ipmg_config_default(ipmg_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->dim = 3;
+  c->degree = 4;
+  c->coarse_cells[0] = c->coarse_cells[1] = c->coarse_cells[2] = 2;
+  c->n_levels = 3;
+  c->h0 = 0.5;
+  c->kernel = IPMG_KERNEL_FULL;
+  c->smoother = IPMG_MULTIPLICATIVE;
+  c->additive_omega = 0.0;
+  c->post_smooth_reverse = 1;
+  c->vcycle_precision = IPMG_FP32;
+  c->penalty_scale = 1.0;
+  c->device = 0;
+  c->cuda_stream = nullptr;
+}
+
+const char* ipmg_last_error(const ipmg_handle* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+ipmg_status ipmg_tables_1d(int k, double penalty_scale, int what, double* out, int cap, int* len) {
+  if (k < 1 || k > 7) return IPMG_ERR_UNSUPPORTED;
+  if (!out || !len || what < 0 || what > 15) return IPMG_ERR_INVALID_ARG;
+  ipmg::FE1D fe = ipmg::build_fe1d(k, penalty_scale);
+  const std::vector<double>* src = nullptr;
+  if (what == 0) src = &fe.nodes;
+  else if (what == 1) src = &fe.M;
+  else if (what == 2) src = &fe.K;
+  else if (what <= 6) src = &fe.LP[what - 3];
+  else if (what <= 10) src = &fe.S[what - 7];
+  else if (what <= 14) src = &fe.lam[what - 11];
+  else src = &fe.P;
+  *len = (int)src->size();
+  if ((int)src->size() > cap) return IPMG_ERR_SIZE_MISMATCH;
+  std::memcpy(out, src->data(), src->size() * sizeof(double));
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
+  if (!cfg || !out) { g_create_error = "null argument"; return IPMG_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (cfg->dim != 2 && cfg->dim != 3) { g_create_error = "dim must be 2 or 3"; return IPMG_ERR_INVALID_ARG; }
+  if (cfg->degree < 1 || cfg->degree > 7) { g_create_error = "degree must be 1..7"; return IPMG_ERR_UNSUPPORTED; }
+  if (cfg->n_levels < 1 || cfg->n_levels > 16 || !(cfg->h0 > 0)) {
+    g_create_error = "n_levels must be 1..16 and h0 > 0";
+    return IPMG_ERR_INVALID_ARG;
+  }
+  for (int a = 0; a < cfg->dim; ++a)
+    if (cfg->coarse_cells[a] != 1 && cfg->coarse_cells[a] != 2) {
+      g_create_error = "coarse_cells must be 1 or 2 per direction";
+      return IPMG_ERR_INVALID_ARG;
+    }
+  if (cfg->kernel != IPMG_KERNEL_FULL) { g_create_error = "only the full kernel is implemented"; return IPMG_ERR_UNSUPPORTED; }
+  if (cfg->smoother != IPMG_MULTIPLICATIVE && cfg->smoother != IPMG_ADDITIVE) {
+    g_create_error = "unknown smoother";
+    return IPMG_ERR_INVALID_ARG;
+  }
+  if (cfg->vcycle_precision != IPMG_FP32 && cfg->vcycle_precision != IPMG_FP64) {
+    g_create_error = "unknown vcycle precision";
+    return IPMG_ERR_INVALID_ARG;
+  }
+  ipmg_handle* h = new (std::nothrow) ipmg_handle();
+  if (!h) { g_create_error = "host allocation failed"; return IPMG_ERR_OUT_OF_MEMORY; }
+  h->cfg = *cfg;
+  if (!(h->cfg.penalty_scale > 0)) h->cfg.penalty_scale = 1.0;
+  h->dim = cfg->dim;
+  h->k = cfg->degree;
+  h->nc = cfg->degree + 1;
+  h->cell = h->dim == 2 ? h->nc * h->nc : h->nc * h->nc * h->nc;
+  h->nlev = cfg->n_levels;
+  h->stream = (cudaStream_t)cfg->cuda_stream;
+  auto bail = [&](ipmg_status st) {
+    g_create_error = h->err;
+    ipmg_destroy(h);
+    return st;
+  };
+  if (cudaSetDevice(cfg->device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return bail(IPMG_ERR_CUDA); }
+  // ---- 1D tables and their upload
+  h->fe = ipmg::build_fe1d(h->k, h->cfg.penalty_scale);
+  h->ks = kernel_set(h->k);
+  {
+    auto t64 = pack_tables<double>(h->fe, h->ks.tab_bytes64);
+    auto t32 = pack_tables<float>(h->fe, h->ks.tab_bytes32);
+    ipmg_status st = h->cuda(h->ks.upload(t64.data(), t32.data(), t64.size(), t32.size()), "table upload");
+    if (st != IPMG_OK) return bail(st);
+  }
+  // ---- hierarchy
+  for (int l = 0; l < h->nlev; ++l) {
+    ipmg::LevelGeom g{};
+    g.n[2] = 1;
+    for (int a = 0; a < h->dim; ++a) g.n[a] = cfg->coarse_cells[a] << l;
+    g.grouped = l >= 1 ? 1 : 0;
+    g.ncells = (long long)g.n[0] * g.n[1] * g.n[2];
+    const double hh = cfg->h0 / double(1LL << l);
+    g.hs = std::pow(hh, h->dim - 2);
+    g.hinv = 1.0 / g.hs;
+    h->geom.push_back(g);
+    h->ndofs.push_back(g.ncells * h->cell);
+    h->hsize.push_back(hh);
+  }
+  // ---- coarse FD tables (global 1D eigenpairs on level 0)
+  h->cdesc.dim = h->dim;
+  h->cdesc.nc = h->nc;
+  h->cdesc.scale = std::pow(cfg->h0, 2 - h->dim);
+  for (int a = 0; a < 3; ++a) {
+    const int n0 = a < h->dim ? cfg->coarse_cells[a] : 1;
+    h->cdesc.n0[a] = n0;
+    h->cdesc.N[a] = a < h->dim ? n0 * h->nc : 1;
+  }
+  for (int a = 0; a < 3; ++a) {
+    std::vector<double> S, lam;
+    const int N = h->cdesc.N[a];
+    if (a < h->dim) {
+      std::vector<double> L, M;
+      ipmg::global_1d(h->fe, h->cdesc.n0[a], L, M);
+      if (!ipmg::gen_eig(N, L, M, S, lam)) { h->err = "coarse eigen-decomposition failed"; return bail(IPMG_ERR_CUDA); }
+    } else {
+      S.assign(1, 1.0);
+      lam.assign(1, 0.0);
+    }
+    std::vector<float> Sf(S.begin(), S.end()), lf(lam.begin(), lam.end());
+    h->cS[0][a] = h->dalloc(S.size() * 8);
+    h->cL[0][a] = h->dalloc(lam.size() * 8);
+    h->cS[1][a] = h->dalloc(S.size() * 4);
+    h->cL[1][a] = h->dalloc(lam.size() * 4);
+    if (!h->cS[0][a] || !h->cL[0][a] || !h->cS[1][a] || !h->cL[1][a]) { h->err = "alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
+    cudaMemcpy(h->cS[0][a], S.data(), S.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(h->cL[0][a], lam.data(), lam.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(h->cS[1][a], Sf.data(), Sf.size() * 4, cudaMemcpyHostToDevice);
+    if (cudaMemcpy(h->cL[1][a], lf.data(), lf.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      h->err = "coarse table upload failed";
+      return bail(IPMG_ERR_CUDA);
+    }
+  }
+  for (int p = 0; p < 2; ++p) h->scratch[p].assign(h->nlev, nullptr);
+  // ---- f == 1 right-hand side pattern per level (w x w (x w) * h^d)
+  h->pattern = (double*)h->dalloc(sizeof(double) * h->cell * h->nlev);
+  h->partial = (double*)h->dalloc(sizeof(double) * ipmg::RED_BLOCKS);
+  h->scal = (double*)h->dalloc(sizeof(double) * 8);
+  if (!h->pattern || !h->partial || !h->scal) { h->err = "alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
+  {
+    std::vector<double> pat((size_t)h->cell * h->nlev);
+    for (int l = 0; l < h->nlev; ++l)
+      for (int e = 0; e < h->cell; ++e) {
+        double v = std::pow(h->hsize[l], h->dim);
+        int r = e;
+        for (int a = 0; a < h->dim; ++a) {
+          v *= h->fe.w[r % h->nc];
+          r /= h->nc;
+        }
+        pat[(size_t)l * h->cell + e] = v;
+      }
+    if (cudaMemcpy(h->pattern, pat.data(), pat.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+      h->err = "pattern upload failed";
+      return bail(IPMG_ERR_CUDA);
+    }
+  }
+  if (cudaMallocHost(&h->hpin, sizeof(double) * 8) != cudaSuccess) { h->err = "pinned alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
+  ipmg_status st = h->ensure_vcycle(h->cfg.vcycle_precision);
+  if (st != IPMG_OK) return bail(st);
+  *out = h;
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_destroy(ipmg_handle* h) {
+  if (!h) return IPMG_OK;
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->hpin) cudaFreeHost(h->hpin);
+  delete h;
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_level_info(const ipmg_handle* h, int level, int64_t* ndofs, int cells[3], double* hsize) {
+  if (!h || level < 0 || level >= h->nlev) return IPMG_ERR_INVALID_ARG;
+  if (ndofs) *ndofs = h->ndofs[level];
+  if (cells)
+    for (int a = 0; a < 3; ++a) cells[a] = h->geom[level].n[a];
+  if (hsize) *hsize = h->hsize[level];
+  return IPMG_OK;
+}
+
+static bool bad_prec(int p) { return p != IPMG_FP64 && p != IPMG_FP32; }
+
+ipmg_status ipmg_vmult(ipmg_handle* h, int level, int precision, const void* x, void* y) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (level < 0 || level >= h->nlev || bad_prec(precision) || !x || !y || x == y)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_vmult: bad level/precision/pointers");
+  if (level == 0 && h->nlev >= 1) {
+    // level 0 may have odd cell counts; the patch-wise operator needs a 2x2(x2) tiling
+    for (int a = 0; a < h->dim; ++a)
+      if (h->geom[0].n[a] % 2) return h->fail(IPMG_ERR_UNSUPPORTED, "ipmg_vmult: level 0 with odd cell count");
+  }
+  return h->cuda(h->ks.vmult(h->dim, precision, x, y, h->geom[level], nullptr, h->stream), "vmult");
+}
+
+ipmg_status ipmg_smooth_colour(ipmg_handle* h, int level, int precision, const void* x_in, const void* b,
+                               void* x_out, int colour) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (level < 1 || level >= h->nlev || bad_prec(precision) || !b || !x_out || x_in == x_out || colour < 0 ||
+      colour >= (1 << h->dim))
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_smooth_colour: bad arguments");
+  return h->smooth_colour(level, precision, x_in, b, x_out, colour);
+}
+
+ipmg_status ipmg_smooth(ipmg_handle* h, int level, int precision, void* x, const void* b, int reverse) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (level < 1 || level >= h->nlev || bad_prec(precision) || !x || !b || x == b)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_smooth: bad arguments");
+  ipmg_status st = h->ensure_scratch(precision, level);
+  if (st != IPMG_OK) return st;
+  if (h->cfg.smoother == IPMG_ADDITIVE) return h->smooth_add(level, precision, x, h->scratch[precision][level], b, false);
+  return h->smooth_mult(level, precision, x, h->scratch[precision][level], b, reverse != 0, false);
+}
+
+ipmg_status ipmg_residual_restrict(ipmg_handle* h, int fine_level, int precision, const void* x, const void* b,
+                                   void* r_c) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !b || !r_c)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_residual_restrict: bad arguments");
+  return h->cuda(h->ks.restrict_(h->dim, precision, x, b, r_c, h->geom[fine_level], h->geom[fine_level - 1], h->stream),
+                 "restrict");
+}
+
+ipmg_status ipmg_prolongate_add(ipmg_handle* h, int fine_level, int precision, const void* e_c, void* x_f) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !e_c || !x_f)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_prolongate_add: bad arguments");
+  return h->cuda(h->ks.prolong(h->dim, precision, e_c, x_f, h->geom[fine_level], h->geom[fine_level - 1], h->stream),
+                 "prolong");
+}
+
+ipmg_status ipmg_coarse_solve(ipmg_handle* h, int precision, const void* b0, void* x0) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (bad_prec(precision) || !b0 || !x0 || b0 == x0) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_coarse_solve: bad arguments");
+  return h->coarse(precision, b0, x0);
+}
+
+ipmg_status ipmg_vcycle(ipmg_handle* h, const double* r, double* z) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (!r || !z || (const void*)r == (const void*)z) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_vcycle: bad pointers");
+  return h->vcycle(r, z, nullptr);
+}
+
+ipmg_status ipmg_rhs(ipmg_handle* h, int level, int kind, double* b) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (level < 0 || level >= h->nlev || kind != 0 || !b) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_rhs: bad arguments");
+  return h->cuda(ipmg::pattern_fill(b, h->pattern + (size_t)level * h->cell, h->cell, h->ndofs[level], h->stream), "rhs");
+}
+
+ipmg_status ipmg_to_cellwise(ipmg_handle* h, int level, int precision, const void* x_lib, void* x_cw) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (level < 0 || level >= h->nlev || bad_prec(precision) || !x_lib || !x_cw || x_lib == x_cw)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_to_cellwise: bad arguments");
+  return h->cuda(ipmg::permute(precision, true, x_lib, x_cw, h->geom[level], h->cell, h->ndofs[level], h->stream), "permute");
+}
+
+ipmg_status ipmg_from_cellwise(ipmg_handle* h, int level, int precision, const void* x_cw, void* x_lib) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (level < 0 || level >= h->nlev || bad_prec(precision) || !x_lib || !x_cw || x_lib == x_cw)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_from_cellwise: bad arguments");
+  return h->cuda(ipmg::permute(precision, false, x_cw, x_lib, h->geom[level], h->cell, h->ndofs[level], h->stream), "permute");
+}
+
+ipmg_status ipmg_synchronize(ipmg_handle* h) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  return h->cuda(cudaStreamSynchronize(h->stream), "synchronize");
+}
+
+ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rtol, int max_it, ipmg_solve_info* info) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (!b || !x || (const void*)b == (const void*)x || !(rtol > 0) || max_it < 1)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_cg_solve: bad arguments");
+  const int L = h->nlev - 1;
+  const long long n = h->ndofs[L];
+  auto t0 = std::chrono::steady_clock::now();
+  if (!h->r) {
+    h->r = (double*)h->dalloc(n * 8);
+    h->p = (double*)h->dalloc(n * 8);
+    h->q = (double*)h->dalloc(n * 8);
+    h->z = (double*)h->dalloc(n * 8);
+    if (!h->r || !h->p || !h->q || !h->z) {
+      h->r = nullptr;
+      return h->fail(IPMG_ERR_OUT_OF_MEMORY, "CG workspace allocation failed");
+    }
+  }
+  cudaStream_t s = h->stream;
+  ipmg_status st;
+#define CK(call, what)                                 \
+  do {                                                 \
+    st = h->cuda((call), what);                        \
+    if (st != IPMG_OK) return st;                      \
+  } while (0)
+  std::vector<double> hist;
+  // slots: 0/1 rz (alternating), 2 pq, 3 rr
+  CK(cudaMemsetAsync(x, 0, n * 8, s), "memset x");
+  CK(cudaMemcpyAsync(h->r, b, n * 8, cudaMemcpyDeviceToDevice, s), "copy r");
+  CK(ipmg::dot_partial(0, 0, h->r, h->r, n, h->partial, s), "dot");
+  CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
+  CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  const double r0 = std::sqrt(h->hpin[0]);
+  hist.push_back(r0);
+  int it = 0;
+  bool conv = (r0 == 0.0);
+  if (!conv) {
+    int cur = 0;
+    st = h->vcycle(h->r, h->z, h->partial);
+    if (st != IPMG_OK) return st;
+    CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
+    CK(cudaMemcpyAsync(h->p, h->z, n * 8, cudaMemcpyDeviceToDevice, s), "copy p");
+    while (it < max_it) {
+      CK(h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, s), "vmult");
+      CK(ipmg::dot_partial(0, 0, h->p, h->q, n, h->partial, s), "dot");
+      CK(ipmg::finalize(h->partial, h->scal + 2, s), "finalize");
+      CK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s), "update");
+      CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
+      CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
+      CK(cudaStreamSynchronize(s), "sync");
+      ++it;
+      const double rn = std::sqrt(h->hpin[0]);
+      hist.push_back(rn);
+      if (rn <= rtol * r0) { conv = true; break; }
+      st = h->vcycle(h->r, h->z, h->partial);
+      if (st != IPMG_OK) return st;
+      CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
+      CK(ipmg::cg_update_p(h->p, h->z, n, h->scal, 1 - cur, cur, s), "update p");
+      cur = 1 - cur;
+    }
+  }
+#undef CK
+  auto t1 = std::chrono::steady_clock::now();
+  if (info) {
+    info->iterations = it;
+    info->rel_residual = r0 > 0 ? hist.back() / r0 : 0.0;
+    info->nu = (it > 0 && info->rel_residual > 0) ? -8.0 * it / std::log10(info->rel_residual) : 0.0;
+    info->seconds = std::chrono::duration<double>(t1 - t0).count();
+    info->history_len = 0;
+    if (info->history && info->history_cap > 0) {
+      const int m = (int)hist.size() < info->history_cap ? (int)hist.size() : info->history_cap;
+      for (int i = 0; i < m; ++i) info->history[i] = hist[i];
+      info->history_len = m;
+    }
+  }
+  if (!conv) return h->fail(IPMG_ERR_NOT_CONVERGED, "ipmg_cg_solve: max_it reached");
+  return IPMG_OK;
+}
+
+}  // extern "C"

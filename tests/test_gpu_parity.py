@@ -1,0 +1,245 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.
+
+Tolerances (north star, BASELINE.json): fp64 operator / smoother / V-cycle /
+CG solution 1e-12 relative; fp32 kernels 1e-5 relative against the fp64 oracle
+evaluated on the same fp32-rounded inputs (reading A18); CG iteration counts
++-1.  Vectors are compared in cell-wise lexicographic order through the
+library's ipmg_to_cellwise (itself checked against the documented layout).
+"""
+import functools
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import assemble, krylov, mesh, multigrid, smoother, transfer  # noqa: E402
+from synth_inputs import uniform  # noqa: E402
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@functools.lru_cache(maxsize=None)
+def handle(dim, k, nl, coarse=None, vprec=1, smoother_kind=0):
+    from paper_2405_18982_b200 import ipmg
+    return ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=vprec, smoother=smoother_kind)
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_levels(dim, k, nl, coarse=None):
+    levels = mesh.hierarchy(dim, nl, coarse)
+    ops = [assemble.assemble(lv, k) for lv in levels]
+    return levels, ops
+
+
+def dev(a, dtype=torch.float64):
+    return torch.tensor(np.asarray(a), dtype=dtype, device="cuda")
+
+
+def to_lib(h, level, v_cw, dtype=torch.float64):
+    """oracle (cell-wise) numpy vector -> library-order device tensor"""
+    src = dev(v_cw, dtype)
+    out = torch.empty_like(src)
+    h.from_cellwise(level, src, out)
+    return out
+
+
+def to_cw(h, level, t):
+    out = torch.empty_like(t)
+    h.to_cellwise(level, t, out)
+    torch.cuda.synchronize()
+    return out.double().cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# (dim, k, n_levels, coarse) -- several CTAs, ragged last CTA, every boundary variant
+CASES = [(2, 1, 4, None), (2, 2, 4, None), (2, 3, 4, None), (2, 4, 3, None), (2, 5, 3, None),
+         (2, 6, 3, None), (2, 7, 3, None), (2, 3, 3, (2, 1)), (3, 1, 3, None), (3, 2, 3, None),
+         (3, 3, 2, None), (3, 4, 2, None), (3, 5, 2, None), (3, 6, 2, None), (3, 7, 2, None),
+         (3, 2, 3, (2, 1, 2))]
+IDS = ["d%dk%dL%d%s" % (c[0], c[1], c[2], "" if c[3] is None else "c" + "".join(map(str, c[3]))) for c in CASES]
+
+
+def test_layout_permutation_matches_documented_formula():
+    _need_gpu()
+    dim, k, nl = 3, 2, 3
+    h = handle(dim, k, nl)
+    L = nl - 1
+    n, cells, _ = h.level_info(L)
+    nc = k + 1
+    cell = nc ** dim
+    x = dev(np.arange(n, dtype=np.float64))
+    y = torch.empty_like(x)
+    h.to_cellwise(L, x, y)
+    got = y.cpu().numpy()
+    # documented layout (include/ipmg.h): ((parent_lex*2^d + child_lex)*cell + node)
+    exp = np.empty(n)
+    for c in range(cells[0] * cells[1] * cells[2]):
+        cx, cy, cz = c % cells[0], (c // cells[0]) % cells[1], c // (cells[0] * cells[1])
+        plin = (cx // 2) + (cells[0] // 2) * ((cy // 2) + (cells[1] // 2) * (cz // 2))
+        lib = (plin * 8 + (cx & 1) + 2 * (cy & 1) + 4 * (cz & 1)) * cell
+        exp[c * cell:(c + 1) * cell] = np.arange(lib, lib + cell)
+    assert np.array_equal(got, exp)
+    z = torch.empty_like(x)
+    h.from_cellwise(L, y, z)
+    assert torch.equal(z, x)
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_vmult(case):
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle(dim, k, nl, coarse)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    for L in range(1, nl):
+        A = ops[L]
+        x = uniform(A.shape[0], seed=10 + L)
+        y_ref = A @ x
+        for dtype, tol in ((torch.float64, 1e-12), (torch.float32, 1e-5)):
+            xr = np.asarray(torch.tensor(x, dtype=dtype).double())
+            xl = to_lib(h, L, x, dtype)
+            yl = torch.empty_like(xl)
+            h.vmult(L, xl, yl)
+            got = to_cw(h, L, yl)
+            ref = A @ xr
+            assert rel(got, ref) <= tol, (L, dtype, rel(got, ref))
+    assert y_ref is not None
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_smoother_colours_and_step(case):
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle(dim, k, nl, coarse)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    L = nl - 1
+    A = ops[L]
+    S = smoother.PatchSmoother(levels[L], k, A)
+    x = uniform(A.shape[0], seed=21)
+    b = uniform(A.shape[0], seed=22)
+    for dtype, tol in ((torch.float64, 1e-12), (torch.float32, 1e-5)):
+        xr = np.asarray(torch.tensor(x, dtype=dtype).double())
+        br = np.asarray(torch.tensor(b, dtype=dtype).double())
+        xl, bl = to_lib(h, L, x, dtype), to_lib(h, L, b, dtype)
+        for c in range(2 ** dim):
+            out = torch.empty_like(xl)
+            h.smooth_colour(L, xl, bl, out, c)
+            ref = xr.copy()
+            for idx, delta in S.local_solves(c, br - A @ xr):
+                ref[idx] += delta
+            assert rel(to_cw(h, L, out), ref) <= tol, (c, dtype)
+        # x_in = NULL (zero start)
+        out = torch.empty_like(xl)
+        h.smooth_colour(L, None, bl, out, 0)
+        ref = np.zeros_like(xr)
+        for idx, delta in S.local_solves(0, br):
+            ref[idx] += delta
+        assert rel(to_cw(h, L, out), ref) <= tol
+        for rev in (False, True):
+            xs = xl.clone()
+            h.smooth(L, xs, bl, reverse=rev)
+            ref = S.smooth(xr, br, reverse=rev)
+            assert rel(to_cw(h, L, xs), ref) <= tol, (rev, dtype)
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_transfers_and_coarse(case):
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle(dim, k, nl, coarse)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    for L in range(1, nl):
+        P = transfer.prolongation(levels[L - 1], levels[L], k)
+        A = ops[L]
+        x = uniform(A.shape[0], seed=31)
+        b = uniform(A.shape[0], seed=32)
+        e = uniform(P.shape[1], seed=33)
+        for dtype, tol in ((torch.float64, 1e-12), (torch.float32, 1e-5)):
+            xr = np.asarray(torch.tensor(x, dtype=dtype).double())
+            br = np.asarray(torch.tensor(b, dtype=dtype).double())
+            er = np.asarray(torch.tensor(e, dtype=dtype).double())
+            xl, bl = to_lib(h, L, x, dtype), to_lib(h, L, b, dtype)
+            rc = torch.empty(P.shape[1], dtype=dtype, device="cuda")
+            h.residual_restrict(L, xl, bl, rc)
+            assert rel(to_cw(h, L - 1, rc), P.T @ (br - A @ xr)) <= tol, (L, dtype)
+            h.residual_restrict(L, None, bl, rc)
+            assert rel(to_cw(h, L - 1, rc), P.T @ br) <= tol
+            xf = xl.clone()
+            h.prolongate_add(L, to_lib(h, L - 1, e, dtype), xf)
+            assert rel(to_cw(h, L, xf), xr + P @ er) <= tol, (L, dtype)
+    A0 = ops[0].toarray()
+    b0 = uniform(A0.shape[0], seed=34)
+    for dtype, tol in ((torch.float64, 1e-12), (torch.float32, 1e-5)):
+        b0r = np.asarray(torch.tensor(b0, dtype=dtype).double())
+        x0 = torch.empty(A0.shape[0], dtype=dtype, device="cuda")
+        h.coarse_solve(to_lib(h, 0, b0, dtype), x0)
+        ref = np.linalg.solve(A0, b0r)
+        # fp32: FD in single precision, conditioning of A_0 enters
+        assert rel(to_cw(h, 0, x0), ref) <= (tol if dtype == torch.float64 else 2e-5), dtype
+
+
+@pytest.mark.parametrize("case", [(2, 2, 4, None), (2, 7, 3, None), (3, 3, 3, None), (3, 2, 3, (2, 1, 2))],
+                         ids=["d2k2", "d2k7", "d3k3", "d3k2c212"])
+@pytest.mark.parametrize("vprec", [0, 1], ids=["fp64", "fp32"])
+def test_vcycle(case, vprec):
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle(dim, k, nl, coarse, vprec)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    V = multigrid.VCycle(dim, k, nl, n0=coarse, operators=ops)
+    L = nl - 1
+    r = uniform(ops[L].shape[0], seed=41)
+    z = torch.empty(len(r), dtype=torch.float64, device="cuda")
+    h.vcycle(to_lib(h, L, r), z)
+    tol = 1e-12 if vprec == 0 else 1e-5
+    assert rel(to_cw(h, L, z), V(r)) <= tol
+
+
+@pytest.mark.parametrize("smk", [0, 1], ids=["mult", "add"])
+def test_vcycle_additive_and_multiplicative_fp64(smk):
+    _need_gpu()
+    dim, k, nl = 2, 3, 4
+    h = handle(dim, k, nl, None, 0, smk)
+    levels, ops = oracle_levels(dim, k, nl)
+    V = multigrid.VCycle(dim, k, nl, operators=ops, smoother="additive" if smk else "multiplicative")
+    r = uniform(ops[-1].shape[0], seed=42)
+    z = torch.empty(len(r), dtype=torch.float64, device="cuda")
+    h.vcycle(to_lib(h, nl - 1, r), z)
+    assert rel(to_cw(h, nl - 1, z), V(r)) <= 1e-12
+
+
+@pytest.mark.parametrize("case", [(2, 2, 3, None), (2, 5, 4, None), (3, 2, 3, None), (3, 4, 2, None)],
+                         ids=["C1_d2k2", "d2k5", "d3k2", "d3k4"])
+@pytest.mark.parametrize("vprec", [0, 1], ids=["fp64", "mixed"])
+def test_cg_solve(case, vprec):
+    """GMG-CG on f == 1: iterations +-1, solution vs the oracle."""
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle(dim, k, nl, coarse, vprec)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    V = multigrid.VCycle(dim, k, nl, n0=coarse, operators=ops,
+                         dtype=np.float64 if vprec == 0 else np.float32)
+    L = nl - 1
+    b = assemble.rhs(levels[L], k)
+    xo, hist, conv = krylov.pcg(ops[L], b, V, rtol=1e-8)
+    bl = torch.empty(len(b), dtype=torch.float64, device="cuda")
+    h.rhs(L, bl)
+    assert rel(to_cw(h, L, bl), b) <= 1e-14            # rhs kernel vs oracle quadrature
+    x = torch.empty_like(bl)
+    res = h.cg_solve(bl, x, rtol=1e-8, max_it=50)
+    assert res["converged"] and conv
+    assert abs(res["iterations"] - (len(hist) - 1)) <= 1
+    tol = 1e-12 if vprec == 0 else 1e-6
+    if res["iterations"] == len(hist) - 1:
+        assert rel(to_cw(h, L, x), xo) <= tol
+    # true residual of the GPU solution, evaluated by the oracle
+    xg = to_cw(h, L, x)
+    assert np.linalg.norm(b - ops[L] @ xg) <= 1.5e-8 * np.linalg.norm(b)
