@@ -158,6 +158,20 @@ ipmg_status ipmg_from_cellwise(ipmg_handle *h, int level, int precision, const v
 /* Synchronise the handle's stream; returns IPMG_ERR_CUDA on an asynchronous fault. */
 ipmg_status ipmg_synchronize(ipmg_handle *h);
 
+/* Instrumentation.  ipmg_profile(h, 1) clears and enables CUDA-event timing
+ * of every kernel launched on the FINEST level (events recorded on the
+ * handle's stream around each launch); 0 disables.  ipmg_profile_read
+ * synchronises and returns, for kernel_class (0 smoother colour pass,
+ * 1 operator apply / residual, 2 residual+restrict, 3 prolongate+add,
+ * 4 coarse solve, 5 vector kernels, 6 additive colour pass), the number of
+ * recorded launches, their summed device time in ms, and their summed
+ * ALGORITHMIC HBM bytes.  ipmg_launch_count: total
+ * kernels this handle has launched. */
+ipmg_status ipmg_profile(ipmg_handle *h, int enable);
+ipmg_status ipmg_profile_read(ipmg_handle *h, int kernel_class, int64_t *launches, double *total_ms,
+                              double *total_bytes);
+ipmg_status ipmg_launch_count(const ipmg_handle *h, int64_t *launches);
+
 /* One-line diagnostic of the last error on h (or of the last failed create
  * when h is NULL).  Library-owned string. */
 const char *ipmg_last_error(const ipmg_handle *h);

@@ -66,6 +66,9 @@ std::vector<unsigned char> pack_tables(const ipmg::FE1D& fe, size_t bytes) {
 
 }  // namespace
 
+enum KClass { KC_SMOOTH = 0, KC_VMULT = 1, KC_RESTRICT = 2, KC_PROLONG = 3, KC_COARSE = 4, KC_BLAS = 5,
+              KC_ADDITIVE = 6, KC_N = 7 };
+
 struct ipmg_handle {
   ipmg_config cfg{};
   int dim = 3, k = 1, nc = 2, cell = 8, nlev = 1;
@@ -86,6 +89,44 @@ struct ipmg_handle {
   double *partial = nullptr, *scal = nullptr, *hpin = nullptr, *pattern = nullptr;
   std::vector<void*> allocs;
   std::string err;
+  // ---- instrumentation: launch counter and (optional) CUDA-event timing of
+  // the finest-level kernels, per kernel class (ipmg_profile*)
+  long long n_launches = 0;
+  bool prof_on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  struct Rec { int cls; double bytes; };
+  std::vector<Rec> recs;
+
+  template <class F>
+  ipmg_status run(int cls, int level, double bytes, int nlaunch, F&& f, const char* what) {
+    n_launches += nlaunch;
+    const bool rec = prof_on && level == nlev - 1;
+    std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+    if (rec) {
+      if (recs.size() == ev_pool.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> p;
+        cudaEventCreate(&p.first);
+        cudaEventCreate(&p.second);
+        ev_pool.push_back(p);
+      }
+      ev = &ev_pool[recs.size()];
+      cudaEventRecord(ev->first, stream);
+    }
+    cudaError_t e = f();
+    if (rec) {
+      cudaEventRecord(ev->second, stream);
+      recs.push_back(Rec{cls, bytes});
+    }
+    return cuda(e, what);
+  }
+  // algorithmic HBM bytes of one smoother colour pass:
+  // covered dofs read b and x_in and write x_out, uncovered dofs are copied
+  double smooth_bytes(int level, int prec, int colour, bool has_x) const {
+    long long covered = 1;
+    for (int a = 0; a < dim; ++a) covered *= ((colour >> a) & 1) ? geom[level].n[a] - 2 : geom[level].n[a];
+    const double cov = (double)covered * cell, unc = (double)ndofs[level] - cov;
+    return esize(prec) * (cov * (2 + (has_x ? 1 : 0)) + unc * (1 + (has_x ? 1 : 0)));
+  }
 
   ipmg_status fail(ipmg_status st, const std::string& msg) {
     err = msg;
@@ -125,7 +166,8 @@ struct ipmg_handle {
 
   // ------------------------------------------------------------ building blocks
   ipmg_status smooth_colour(int level, int prec, const void* xi, const void* b, void* xo, int colour) {
-    return cuda(ks.smooth(dim, prec, xi, b, xo, geom[level], colour, stream), "smooth_colour");
+    return run(KC_SMOOTH, level, smooth_bytes(level, prec, colour, xi != nullptr), 1,
+               [&] { return ks.smooth(dim, prec, xi, b, xo, geom[level], colour, stream); }, "smooth_colour");
   }
   // multiplicative step: passes ping-pong between x and other; 2^d passes -> ends in x
   ipmg_status smooth_mult(int level, int prec, void* x, void* other, const void* b, bool reverse, bool x_is_zero) {
@@ -147,7 +189,8 @@ struct ipmg_handle {
   ipmg_status smooth_add(int level, int prec, void* x, void* rbuf, const void* b, bool x_is_zero) {
     const void* r = b;
     if (!x_is_zero) {
-      ipmg_status st = cuda(ks.vmult(dim, prec, x, rbuf, geom[level], b, stream), "residual");
+      ipmg_status st = run(KC_VMULT, level, 3.0 * esize(prec) * ndofs[level], 1,
+                           [&] { return ks.vmult(dim, prec, x, rbuf, geom[level], b, stream); }, "residual");
       if (st != IPMG_OK) return st;
       r = rbuf;
     } else {
@@ -155,7 +198,8 @@ struct ipmg_handle {
       if (st != IPMG_OK) return st;
     }
     for (int c = 0; c < (1 << dim); ++c) {
-      ipmg_status st = cuda(ks.additive(dim, prec, r, x, geom[level], c, omega(), stream), "additive");
+      ipmg_status st = run(KC_ADDITIVE, level, 3.0 * esize(prec) * ndofs[level] / (1 << dim), 1,
+                           [&] { return ks.additive(dim, prec, r, x, geom[level], c, omega(), stream); }, "additive");
       if (st != IPMG_OK) return st;
     }
     return IPMG_OK;
@@ -163,7 +207,8 @@ struct ipmg_handle {
   ipmg_status coarse(int prec, const void* b, void* x) {
     const void* S[3] = {cS[prec][0], cS[prec][1], cS[prec][2]};
     const void* L[3] = {cL[prec][0], cL[prec][1], cL[prec][2]};
-    return cuda(ipmg::coarse_solve(prec, b, x, cdesc, S, L, stream), "coarse_solve");
+    return run(KC_COARSE, 0, 2.0 * esize(prec) * ndofs[0], 1,
+               [&] { return ipmg::coarse_solve(prec, b, x, cdesc, S, L, stream); }, "coarse_solve");
   }
   // one V-cycle on level l of the workspace of precision prec: input vb[l],
   // output vx1[l]
@@ -179,11 +224,13 @@ struct ipmg_handle {
     else st = smooth_mult(l, prec, x1, x0, b, false, true);
     if (st != IPMG_OK) return st;
     // (2) coarse-grid correction x1 += P P_{l-1}^{-1} P^T (b - A x1)
-    st = cuda(ks.restrict_(dim, prec, x1, b, vb[prec][l - 1], geom[l], geom[l - 1], stream), "restrict");
+    st = run(KC_RESTRICT, l, esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]), 1,
+             [&] { return ks.restrict_(dim, prec, x1, b, vb[prec][l - 1], geom[l], geom[l - 1], stream); }, "restrict");
     if (st != IPMG_OK) return st;
     st = vcycle_level(l - 1, prec);
     if (st != IPMG_OK) return st;
-    st = cuda(ks.prolong(dim, prec, vx1[prec][l - 1], x1, geom[l], geom[l - 1], stream), "prolong");
+    st = run(KC_PROLONG, l, esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]), 1,
+             [&] { return ks.prolong(dim, prec, vx1[prec][l - 1], x1, geom[l], geom[l - 1], stream); }, "prolong");
     if (st != IPMG_OK) return st;
     // (3) post-smoothing (colours reversed for a symmetric V-cycle, reading A7)
     if (additive) return smooth_add(l, prec, x1, x0, b, false);
@@ -194,15 +241,20 @@ struct ipmg_handle {
     const int L = nlev - 1;
     ipmg_status st = ensure_vcycle(prec);
     if (st != IPMG_OK) return st;
-    st = cuda(ipmg::cast(0, prec, r, vb[prec][L], ndofs[L], stream), "cast in");
+    st = run(KC_BLAS, L, (8.0 + esize(prec)) * ndofs[L], prec == 0 ? 0 : 1,
+             [&] { return ipmg::cast(0, prec, r, vb[prec][L], ndofs[L], stream); }, "cast in");
     if (st != IPMG_OK) return st;
     st = vcycle_level(L, prec);
     if (st != IPMG_OK) return st;
     if (rz_partial && prec == IPMG_FP32)
-      return cuda(ipmg::cast_f2d_dot((const float*)vx1[prec][L], z, r, ndofs[L], rz_partial, stream), "cast out");
-    st = cuda(ipmg::cast(prec, 0, vx1[prec][L], z, ndofs[L], stream), "cast out");
+      return run(KC_BLAS, L, 20.0 * ndofs[L], 1,
+                 [&] { return ipmg::cast_f2d_dot((const float*)vx1[prec][L], z, r, ndofs[L], rz_partial, stream); },
+                 "cast out");
+    st = run(KC_BLAS, L, (8.0 + esize(prec)) * ndofs[L], prec == 0 ? 0 : 1,
+             [&] { return ipmg::cast(prec, 0, vx1[prec][L], z, ndofs[L], stream); }, "cast out");
     if (st != IPMG_OK || !rz_partial) return st;
-    return cuda(ipmg::dot_partial(0, 0, r, z, ndofs[L], rz_partial, stream), "dot");
+    return run(KC_BLAS, L, 16.0 * ndofs[L], 1,
+               [&] { return ipmg::dot_partial(0, 0, r, z, ndofs[L], rz_partial, stream); }, "dot");
   }
 };
 
@@ -374,6 +426,10 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
 
 ipmg_status ipmg_destroy(ipmg_handle* h) {
   if (!h) return IPMG_OK;
+  for (auto& e : h->ev_pool) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   for (void* p : h->allocs) cudaFree(p);
   if (h->hpin) cudaFreeHost(h->hpin);
   delete h;
@@ -400,7 +456,8 @@ ipmg_status ipmg_vmult(ipmg_handle* h, int level, int precision, const void* x, 
     for (int a = 0; a < h->dim; ++a)
       if (h->geom[0].n[a] % 2) return h->fail(IPMG_ERR_UNSUPPORTED, "ipmg_vmult: level 0 with odd cell count");
   }
-  return h->cuda(h->ks.vmult(h->dim, precision, x, y, h->geom[level], nullptr, h->stream), "vmult");
+  return h->run(KC_VMULT, level, 2.0 * h->esize(precision) * h->ndofs[level], 1,
+                [&] { return h->ks.vmult(h->dim, precision, x, y, h->geom[level], nullptr, h->stream); }, "vmult");
 }
 
 ipmg_status ipmg_smooth_colour(ipmg_handle* h, int level, int precision, const void* x_in, const void* b,
@@ -427,16 +484,23 @@ ipmg_status ipmg_residual_restrict(ipmg_handle* h, int fine_level, int precision
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !b || !r_c)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_residual_restrict: bad arguments");
-  return h->cuda(h->ks.restrict_(h->dim, precision, x, b, r_c, h->geom[fine_level], h->geom[fine_level - 1], h->stream),
-                 "restrict");
+  return h->run(KC_RESTRICT, fine_level, h->esize(precision) * (2.0 * h->ndofs[fine_level] + h->ndofs[fine_level - 1]), 1,
+                [&] {
+                  return h->ks.restrict_(h->dim, precision, x, b, r_c, h->geom[fine_level], h->geom[fine_level - 1],
+                                         h->stream);
+                },
+                "restrict");
 }
 
 ipmg_status ipmg_prolongate_add(ipmg_handle* h, int fine_level, int precision, const void* e_c, void* x_f) {
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !e_c || !x_f)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_prolongate_add: bad arguments");
-  return h->cuda(h->ks.prolong(h->dim, precision, e_c, x_f, h->geom[fine_level], h->geom[fine_level - 1], h->stream),
-                 "prolong");
+  return h->run(KC_PROLONG, fine_level, h->esize(precision) * (2.0 * h->ndofs[fine_level] + h->ndofs[fine_level - 1]), 1,
+                [&] {
+                  return h->ks.prolong(h->dim, precision, e_c, x_f, h->geom[fine_level], h->geom[fine_level - 1], h->stream);
+                },
+                "prolong");
 }
 
 ipmg_status ipmg_coarse_solve(ipmg_handle* h, int precision, const void* b0, void* x0) {
@@ -454,6 +518,7 @@ ipmg_status ipmg_vcycle(ipmg_handle* h, const double* r, double* z) {
 ipmg_status ipmg_rhs(ipmg_handle* h, int level, int kind, double* b) {
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 0 || level >= h->nlev || kind != 0 || !b) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_rhs: bad arguments");
+  h->n_launches += 1;
   return h->cuda(ipmg::pattern_fill(b, h->pattern + (size_t)level * h->cell, h->cell, h->ndofs[level], h->stream), "rhs");
 }
 
@@ -461,6 +526,7 @@ ipmg_status ipmg_to_cellwise(ipmg_handle* h, int level, int precision, const voi
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 0 || level >= h->nlev || bad_prec(precision) || !x_lib || !x_cw || x_lib == x_cw)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_to_cellwise: bad arguments");
+  h->n_launches += 1;
   return h->cuda(ipmg::permute(precision, true, x_lib, x_cw, h->geom[level], h->cell, h->ndofs[level], h->stream), "permute");
 }
 
@@ -468,6 +534,7 @@ ipmg_status ipmg_from_cellwise(ipmg_handle* h, int level, int precision, const v
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 0 || level >= h->nlev || bad_prec(precision) || !x_lib || !x_cw || x_lib == x_cw)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_from_cellwise: bad arguments");
+  h->n_launches += 1;
   return h->cuda(ipmg::permute(precision, false, x_cw, x_lib, h->geom[level], h->cell, h->ndofs[level], h->stream), "permute");
 }
 
@@ -504,6 +571,7 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
   // slots: 0/1 rz (alternating), 2 pq, 3 rr
   CK(cudaMemsetAsync(x, 0, n * 8, s), "memset x");
   CK(cudaMemcpyAsync(h->r, b, n * 8, cudaMemcpyDeviceToDevice, s), "copy r");
+  h->n_launches += 2;
   CK(ipmg::dot_partial(0, 0, h->r, h->r, n, h->partial, s), "dot");
   CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
   CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
@@ -516,10 +584,14 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     int cur = 0;
     st = h->vcycle(h->r, h->z, h->partial);
     if (st != IPMG_OK) return st;
+    h->n_launches += 1;
     CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
     CK(cudaMemcpyAsync(h->p, h->z, n * 8, cudaMemcpyDeviceToDevice, s), "copy p");
     while (it < max_it) {
-      CK(h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, s), "vmult");
+      st = h->run(KC_VMULT, L, 16.0 * n, 1,
+                  [&] { return h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, s); }, "vmult");
+      if (st != IPMG_OK) return st;
+      h->n_launches += 4;
       CK(ipmg::dot_partial(0, 0, h->p, h->q, n, h->partial, s), "dot");
       CK(ipmg::finalize(h->partial, h->scal + 2, s), "finalize");
       CK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s), "update");
@@ -532,6 +604,7 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       if (rn <= rtol * r0) { conv = true; break; }
       st = h->vcycle(h->r, h->z, h->partial);
       if (st != IPMG_OK) return st;
+      h->n_launches += 2;
       CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
       CK(ipmg::cg_update_p(h->p, h->z, n, h->scal, 1 - cur, cur, s), "update p");
       cur = 1 - cur;
@@ -552,6 +625,41 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     }
   }
   if (!conv) return h->fail(IPMG_ERR_NOT_CONVERGED, "ipmg_cg_solve: max_it reached");
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_profile(ipmg_handle* h, int enable) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  h->prof_on = enable != 0;
+  if (h->prof_on) h->recs.clear();
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_profile_read(ipmg_handle* h, int kernel_class, int64_t* launches, double* total_ms,
+                              double* total_bytes) {
+  if (!h || kernel_class < 0 || kernel_class >= KC_N) return IPMG_ERR_INVALID_ARG;
+  ipmg_status st = h->cuda(cudaStreamSynchronize(h->stream), "profile sync");
+  if (st != IPMG_OK) return st;
+  int64_t n = 0;
+  double ms = 0.0, by = 0.0;
+  for (size_t i = 0; i < h->recs.size(); ++i) {
+    if (h->recs[i].cls != kernel_class) continue;
+    float t = 0.f;
+    st = h->cuda(cudaEventElapsedTime(&t, h->ev_pool[i].first, h->ev_pool[i].second), "event time");
+    if (st != IPMG_OK) return st;
+    ++n;
+    ms += t;
+    by += h->recs[i].bytes;
+  }
+  if (launches) *launches = n;
+  if (total_ms) *total_ms = ms;
+  if (total_bytes) *total_bytes = by;
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_launch_count(const ipmg_handle* h, int64_t* launches) {
+  if (!h || !launches) return IPMG_ERR_INVALID_ARG;
+  *launches = h->n_launches;
   return IPMG_OK;
 }
 

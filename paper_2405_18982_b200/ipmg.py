@@ -24,7 +24,10 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "SIZE_MISMATCH", 4: "O
 EXPORTS = ["ipmg_config_default", "ipmg_create", "ipmg_destroy", "ipmg_level_info", "ipmg_vmult",
            "ipmg_smooth", "ipmg_smooth_colour", "ipmg_residual_restrict", "ipmg_prolongate_add",
            "ipmg_coarse_solve", "ipmg_vcycle", "ipmg_cg_solve", "ipmg_rhs", "ipmg_to_cellwise",
-           "ipmg_from_cellwise", "ipmg_synchronize", "ipmg_last_error", "ipmg_tables_1d"]
+           "ipmg_from_cellwise", "ipmg_synchronize", "ipmg_last_error", "ipmg_tables_1d",
+           "ipmg_profile", "ipmg_profile_read", "ipmg_launch_count"]
+
+KERNEL_CLASSES = {"smooth": 0, "vmult": 1, "restrict": 2, "prolong": 3, "coarse": 4, "blas": 5, "additive": 6}
 
 
 class Config(ctypes.Structure):
@@ -74,6 +77,10 @@ def load():
         "ipmg_synchronize": (i, [vp]),
         "ipmg_last_error": (ctypes.c_char_p, [vp]),
         "ipmg_tables_1d": (i, [i, d, i, ctypes.POINTER(ctypes.c_double), i, ctypes.POINTER(ctypes.c_int)]),
+        "ipmg_profile": (i, [vp, i]),
+        "ipmg_profile_read": (i, [vp, i, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double)]),
+        "ipmg_launch_count": (i, [vp, ctypes.POINTER(ctypes.c_int64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -246,6 +253,24 @@ class Handle:
         p = self._prec(x_cw)
         self._vec(x_lib, level, p), self._vec(x_cw, level, p)
         self._check(self.lib.ipmg_from_cellwise(self.h, level, p, _ptr(x_cw), _ptr(x_lib)), "from_cellwise")
+
+    def profile(self, enable=True):
+        self._check(self.lib.ipmg_profile(self.h, int(enable)), "profile")
+
+    def profile_read(self, kernel_class):
+        """(launches, total_ms, total_algorithmic_bytes) of a kernel class on the finest level."""
+        n = ctypes.c_int64(0)
+        ms = ctypes.c_double(0)
+        by = ctypes.c_double(0)
+        cls = KERNEL_CLASSES.get(kernel_class, kernel_class)
+        self._check(self.lib.ipmg_profile_read(self.h, cls, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)),
+                    "profile_read")
+        return n.value, ms.value, by.value
+
+    def launch_count(self):
+        n = ctypes.c_int64(0)
+        self._check(self.lib.ipmg_launch_count(self.h, ctypes.byref(n)), "launch_count")
+        return n.value
 
     def synchronize(self):
         self._check(self.lib.ipmg_synchronize(self.h), "synchronize")

@@ -1,0 +1,94 @@
+"""Summarise ncu reports into a small JSON/markdown table (run here, no GPU).
+
+  python profiles/ncu_summary.py gpurun_out/prof_smooth_r01.ncu-rep [...] > profiles/xxx.md
+  python profiles/ncu_summary.py --launches gpurun_out/launches_r01.csv
+
+Per kernel launch: duration, dram bytes (read+write), achieved DRAM %, issue
+slots, registers, occupancy, FP32/FP64 pipe utilisation, shared-memory bank
+conflicts (excess wavefronts) -- the evidence DESIGN.md cites.
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+WANT = [
+    ("Duration", "gpu__time_duration.sum"),
+    ("DRAM read", "dram__bytes_read.sum"),
+    ("DRAM write", "dram__bytes_write.sum"),
+    ("DRAM %", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("SM busy %", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("Issue active %", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
+    ("Registers", "launch__registers_per_thread"),
+    ("Occupancy %", "sm__warps_active.avg.pct_of_peak_sustained_active"),
+    ("FMA pipe %", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("FP64 pipe %", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("Inst executed", "smsp__inst_executed.sum"),
+    ("FFMA thread-inst", "sm__sass_thread_inst_executed_op_ffma_pred_on.sum"),
+    ("DFMA thread-inst", "sm__sass_thread_inst_executed_op_dfma_pred_on.sum"),
+    ("smem ld bank conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"),
+    ("smem st bank conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"),
+    ("L2 hit %", "lts__t_sector_hit_rate.pct"),
+]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], stdout=subprocess.PIPE,
+                         stderr=subprocess.DEVNULL, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    units = rows[1]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        res.append((d, u))
+    return res
+
+
+def summarise(rep):
+    lines = ["### %s" % rep, "", "| launch | kernel | " + " | ".join(w[0] for w in WANT) + " |",
+             "|---" * (len(WANT) + 2) + "|"]
+    for i, (d, u) in enumerate(raw(rep)):
+        name = d.get("Kernel Name", "?")[:48]
+        vals = []
+        for label, m in WANT:
+            v = d.get(m, "n/a")
+            unit = u.get(m, "")
+            vals.append("%s %s" % (v, unit) if v != "n/a" else "n/a")
+        lines.append("| %d | %s | %s |" % (i, name, " | ".join(vals)))
+    return "\n".join(lines) + "\n"
+
+
+def launches(path):
+    """Per-kernel share of the device time in an ncu --metrics gpu__time_duration.sum CSV."""
+    text = open(path).read()
+    start = text.find('"ID"')
+    rows = list(csv.DictReader(io.StringIO(text[start:])))
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"].split("(")[0]
+        v = float(r["Metric Value"].replace(",", ""))
+        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r.get("Metric Unit", "us"), 1.0)
+        tot[name] += v * scale
+        cnt[name] += 1
+    T = sum(tot.values())
+    out = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        out.append("| %s | %d | %.1f | %.1f%% |" % (k, cnt[k], v, 100 * v / T))
+    out.append("| **total** | %d | %.1f | 100%% |" % (sum(cnt.values()), T))
+    return "\n".join(out) + "\n"
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--launches":
+        for p in sys.argv[2:]:
+            print("### %s\n" % p)
+            print(launches(p))
+    else:
+        for p in sys.argv[1:]:
+            print(summarise(p))
