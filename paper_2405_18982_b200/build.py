@@ -44,18 +44,23 @@ def _run(cmd, log):
     return p.stdout
 
 
-def build(force=False, verbose=False, jobs=None):
-    os.makedirs(OBJ, exist_ok=True)
+def build(force=False, verbose=False, jobs=None, defines=(), tag=""):
+    """defines: extra -D flags (tuning experiments); tag: build into _build<tag>/ and
+    libipmg<tag>.so (load it with IPMG_LIB=...)."""
+    obj_dir = OBJ + tag
+    lib = LIB if not tag else os.path.join(HERE, "libipmg%s.so" % tag)
+    os.makedirs(obj_dir, exist_ok=True)
+    cuflags = CUFLAGS + ["-D" + d for d in defines]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "ipmg.h")]
     tasks = []
     for s in SOURCES_CU:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(OBJ, s + ".o")
+        obj = os.path.join(obj_dir, s + ".o")
         if force or _stale(obj, [src] + hdrs):
-            tasks.append(([NVCC] + CUFLAGS + ["-c", src, "-o", obj], obj + ".log"))
+            tasks.append(([NVCC] + cuflags + ["-c", src, "-o", obj], obj + ".log"))
     for s in SOURCES_CXX:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(OBJ, s + ".o")
+        obj = os.path.join(obj_dir, s + ".o")
         if force or _stale(obj, [src] + hdrs):
             tasks.append((["g++"] + CXXFLAGS + ["-c", src, "-o", obj], obj + ".log"))
     jobs = jobs or max(1, os.cpu_count() or 1)
@@ -64,12 +69,14 @@ def build(force=False, verbose=False, jobs=None):
     if verbose:
         for o in outs:
             sys.stdout.write(o)
-    objs = [os.path.join(OBJ, s + ".o") for s in SOURCES_CU + SOURCES_CXX]
-    if force or tasks or _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs, os.path.join(OBJ, "link.log"))
-    return LIB
+    objs = [os.path.join(obj_dir, s + ".o") for s in SOURCES_CU + SOURCES_CXX]
+    if force or tasks or _stale(lib, objs):
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs, os.path.join(obj_dir, "link.log"))
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    tags = [a[6:] for a in sys.argv[1:] if a.startswith("--tag=")]
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, defines=defs,
+                tag=tags[0] if tags else ""))

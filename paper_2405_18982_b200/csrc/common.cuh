@@ -39,24 +39,37 @@ __host__ __device__ __forceinline__ long long cell_offset_cells(const LevelGeom&
 
 // Device-side 1D tables for degree K in precision T (unit h); one instance per
 // precision lives in __constant__ memory of each per-degree translation unit.
+// Rows are padded to a multiple of 4 entries and 16-byte aligned so that a
+// kernel walking a row with compile-time indices loads 4 (fp32) / 2 (fp64)
+// constants per uniform-register load (LDCU.128).  Every matrix is stored in
+// the orientation it is applied in (out[i] = sum_j A[i][j] in[j], j contiguous).
 template <int K, typename T>
 struct TabData {
   static constexpr int NC = K + 1, NP = 2 * (K + 1);
-  T M[NC][NC];          // cell mass
-  T LP[4][NP][NP];      // 2-cell patch stiffness + face terms, variant v
-  T S[4][NP][NP];       // eigenvectors, S[v][node][mode]
-  T lam[4][NP];         // eigenvalues
-  T d0[NC], d1[NC];     // phi_j'(0), phi_j'(1)
-  T P[NP][NC];          // prolongation (patch-lex fine node, coarse node)
-  T w[NC];              // int phi_i
-  T gamma;              // unit penalty 2k(k+1)*scale
+  static constexpr int RC = (NC + 3) & ~3, RP = (NP + 3) & ~3;   // padded row lengths
+  alignas(16) T M[NC][RC];          // cell mass
+  alignas(16) T LP[4][NP][RP];      // 2-cell patch stiffness + face terms, variant v
+  alignas(16) T S[4][NP][RP];       // eigenvectors, S[v][node][mode]
+  alignas(16) T ST[4][NP][RP];      // transposed eigenvectors, ST[v][mode][node]
+  alignas(16) T MS[4][NP][RP];      // M^P S = (S^T M^P)^T: face arrays of directions already in eigen-space
+  alignas(16) T CF[4][RP];          // face coupling coefficients along the normal (C x_ext):
+                                    // 0 low/u, 1 low/u', 2 high/u, 3 high/u'  (see face_* kernels)
+  alignas(16) T CH[4][4][RP];       // the same in eigen-space: CH[v][kind][m] = sum_i S[v][i][m] CF[kind][i]
+  alignas(16) T lam[4][RP];         // eigenvalues
+  alignas(16) T d0[RC];             // phi_j'(0)
+  alignas(16) T d1[RC];             // phi_j'(1)
+  alignas(16) T P[NP][RC];          // prolongation (patch-lex fine node, coarse node)
+  alignas(16) T PT[NC][RP];         // restriction = P^T
+  alignas(16) T w[RC];              // int phi_i
+  T gamma;                          // unit penalty 2k(k+1)*scale
 };
+
+struct FE1D;
 
 // Per-degree launcher table exported by each kernels_k<K>.cu.
 struct KernelSet {
   int k;
-  cudaError_t (*upload)(const void* tab64, const void* tab32, size_t bytes64, size_t bytes32);
-  size_t tab_bytes64, tab_bytes32;
+  cudaError_t (*upload)(const FE1D& fe);   // fill and upload the __constant__ tables
   // all launchers: prec 0 = double, 1 = float; dim 2 or 3
   cudaError_t (*vmult)(int dim, int prec, const void* x, void* y, const LevelGeom& g,
                        const void* b_minus, cudaStream_t s);

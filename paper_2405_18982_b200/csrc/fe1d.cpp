@@ -288,6 +288,37 @@ FE1D build_fe1d(int k, double penalty_scale) {
     fe.LP[var] = sipg_chain(fe, 2, var & 1, var & 2);
     gen_eig(np, fe.LP[var], fe.MP, fe.S[var], fe.lam[var]);
   }
+  // The interior patch problem (variant 0) is symmetric under the reflection
+  // i -> np-1-i, so every eigenvector is even or odd.  Order its modes as
+  // [even modes (ascending) | odd modes (ascending)] and symmetrise exactly;
+  // the kernels then apply S and S^T with half-size even/odd products.
+  {
+    std::vector<int> ev, od;
+    for (int m = 0; m < np; ++m) {
+      double se = 0.0, so = 0.0;
+      for (int i = 0; i < np; ++i) {
+        se += std::fabs(fe.S[0][i * np + m] - fe.S[0][(np - 1 - i) * np + m]);
+        so += std::fabs(fe.S[0][i * np + m] + fe.S[0][(np - 1 - i) * np + m]);
+      }
+      (se < so ? ev : od).push_back(m);
+    }
+    if ((int)ev.size() == np / 2 && (int)od.size() == np / 2) {
+      std::vector<double> S2(np * np), l2(np);
+      for (int k = 0; k < np; ++k) {
+        const int m = k < np / 2 ? ev[k] : od[k - np / 2];
+        const double sg = k < np / 2 ? 1.0 : -1.0;
+        l2[k] = fe.lam[0][m];
+        for (int i = 0; i < np / 2; ++i) {
+          const double a = 0.5 * (fe.S[0][i * np + m] + sg * fe.S[0][(np - 1 - i) * np + m]);
+          S2[i * np + k] = a;
+          S2[(np - 1 - i) * np + k] = sg * a;
+        }
+      }
+      fe.S[0] = S2;
+      fe.lam[0] = l2;
+      fe.even_odd = true;
+    }
+  }
   fe.P.assign(np * nc, 0.0);
   for (int i = 0; i < np; ++i) {
     double x = 0.5 * (fe.nodes[i % nc] + (i / nc));

@@ -28,7 +28,8 @@ struct FE1D {
   std::vector<double> MP;          // patch mass (block diagonal)             (np*np)
   std::vector<double> LP[4];       // patch stiffness + face terms            (np*np)
   std::vector<double> S[4];        // generalized eigenvectors, S[i*np+m] = node i, mode m
-  std::vector<double> lam[4];      // eigenvalues ascending                    (np)
+  std::vector<double> lam[4];      // eigenvalues (variant 0: even modes then odd modes, each ascending)
+  bool even_odd = false;           // variant-0 modes ordered [even | odd] (always true in practice)
   std::vector<double> P;           // prolongation, P[i*nc+j] = phi_j((xi_{i%nc} + i/nc)/2)  (np*nc)
 };
 

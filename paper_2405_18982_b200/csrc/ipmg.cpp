@@ -40,30 +40,6 @@ ipmg::KernelSet kernel_set(int k) {
   }
 }
 
-// Host copy of TabData<K,T> laid out exactly like the device struct.
-template <typename T>
-std::vector<unsigned char> pack_tables(const ipmg::FE1D& fe, size_t bytes) {
-  const int nc = fe.nc, np = fe.np;
-  std::vector<T> v;
-  v.reserve(bytes / sizeof(T));
-  for (int i = 0; i < nc * nc; ++i) v.push_back((T)fe.M[i]);
-  for (int var = 0; var < 4; ++var)
-    for (int i = 0; i < np * np; ++i) v.push_back((T)fe.LP[var][i]);
-  for (int var = 0; var < 4; ++var)
-    for (int i = 0; i < np * np; ++i) v.push_back((T)fe.S[var][i]);
-  for (int var = 0; var < 4; ++var)
-    for (int i = 0; i < np; ++i) v.push_back((T)fe.lam[var][i]);
-  for (int i = 0; i < nc; ++i) v.push_back((T)fe.d0[i]);
-  for (int i = 0; i < nc; ++i) v.push_back((T)fe.d1[i]);
-  for (int i = 0; i < np * nc; ++i) v.push_back((T)fe.P[i]);
-  for (int i = 0; i < nc; ++i) v.push_back((T)fe.w[i]);
-  v.push_back((T)fe.gamma);
-  std::vector<unsigned char> out(bytes, 0);
-  const size_t used = v.size() * sizeof(T);
-  if (used <= bytes) std::memcpy(out.data(), v.data(), used);
-  return out;
-}
-
 }  // namespace
 
 enum KClass { KC_SMOOTH = 0, KC_VMULT = 1, KC_RESTRICT = 2, KC_PROLONG = 3, KC_COARSE = 4, KC_BLAS = 5,
@@ -339,11 +315,13 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   if (cudaSetDevice(cfg->device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return bail(IPMG_ERR_CUDA); }
   // ---- 1D tables and their upload
   h->fe = ipmg::build_fe1d(h->k, h->cfg.penalty_scale);
+  if (!h->fe.even_odd) {   // the interior-patch fast path relies on the reflection symmetry
+    h->err = "interior patch eigenvectors are not even/odd";
+    return bail(IPMG_ERR_UNSUPPORTED);
+  }
   h->ks = kernel_set(h->k);
   {
-    auto t64 = pack_tables<double>(h->fe, h->ks.tab_bytes64);
-    auto t32 = pack_tables<float>(h->fe, h->ks.tab_bytes32);
-    ipmg_status st = h->cuda(h->ks.upload(t64.data(), t32.data(), t64.size(), t32.size()), "table upload");
+    ipmg_status st = h->cuda(h->ks.upload(h->fe), "table upload");
     if (st != IPMG_OK) return bail(st);
   }
   // ---- hierarchy

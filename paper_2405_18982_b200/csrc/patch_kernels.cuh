@@ -2,27 +2,33 @@
 // K (via IPMG_K of the including translation unit) and precision T.
 //
 // One CTA processes PPC vertex patches of one colour.  Each patch is staged in
-// shared memory as a patch-lexicographic tensor of (2(k+1))^d values (row pitch
-// 2(k+1)+1, odd, so x-lines and y-lines are bank-conflict free), loaded and
-// stored with coalesced cooperative copies of whole cell chunks.  Every
-// sum-factorisation step is a "line pass": each thread owns whole 1D lines of
-// the tensor along one direction, reads the line into registers, multiplies it
-// by a 1D matrix whose entries are compile-time indexed __constant__ operands
-// (no load instructions for the matrix), and writes the line back in place.
+// shared memory as a patch-lexicographic tensor of (2(k+1))^d values (odd row
+// pitch; plane and patch pitches padded by a compile-time search so that the
+// line passes are shared-memory bank-conflict free), loaded and stored with
+// coalesced (vectorised where the cell size allows) cooperative copies of
+// whole cell chunks.  Every sum-factorisation step is a "line pass": a thread
+// owns R whole 1D lines of one patch along one direction (R = 2 in fp32, 1 in
+// fp64), reads them into registers, multiplies them by a 1D matrix whose
+// entries are compile-time-indexed __constant__ data (one uniform-register
+// load LDCU.128 feeds 4R FMAs), and writes the lines back in place.
 //
-//  vmult_kernel     y = A x                      PAPER.md:112-138 (Fig. 1 patch-wise
-//                   over colour-0 patches;        integration, Kronecker sum of
-//                   each patch writes only its   PAPER.md:118-126, face terms of
-//                   own cells -> no atomics)      eq. bilinear_form)
-//  smooth_kernel    one colour of Algorithm 1,
-//                   full kernel, in replacement form x_j = A_j^{-1}(b_j - C_j x_ext),
-//                   algebraically identical to x_j + A_j^{-1} R_j(b - A x) because
-//                   A_j = R_j A R_j^T; A_j^{-1} by fast diagonalisation
+//  vmult_kernel     y = A x over colour-0 patches   PAPER.md:112-138 (Fig. 1 patch-wise
+//                   (each patch writes only its      integration), Kronecker sum of
+//                   own cells -> no atomics)         PAPER.md:118-126, face terms of
+//                                                    eq. bilinear_form
+//  smooth_kernel    one colour of Algorithm 1, full kernel, replacement form
+//                   x_j = A_j^{-1}(b_j - C_j x_ext), algebraically identical to
+//                   x_j + A_j^{-1} R_j (b - A x) because A_j = R_j A R_j^T
+//                   (PAPER.md:183-199, 242-257); A_j^{-1} by fast diagonalisation
+//
 //  additive_kernel  x += omega R_j^T A_j^{-1} R_j r over one colour (r precomputed)
 //  restrict_kernel  r_c = P^T (b - A x) per parent cell
 //  prolong_kernel   x_f += P e_c per parent cell
 #pragma once
 #include "common.cuh"
+#include "fe1d.hpp"
+
+#include <cstring>
 
 #ifndef IPMG_K
 #error "IPMG_K must be defined by the including translation unit"
@@ -52,36 +58,161 @@ template <>
 __device__ __forceinline__ const TabData<K, float>& tab<float>() { return c_tab32; }
 
 // ---------------------------------------------------------------- configuration
-template <int D>
+constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// bank multiplicity of one warp-wide access whose per-thread word offsets are
+// base(u) (4-byte words for fp32; 8-byte words for fp64, served per half warp)
+template <typename T, class F>
+constexpr int bank_cost(F base, int nthreads) {
+  int worst = 1;
+  if (sizeof(T) == 4) {
+    for (int b = 0; b < 32; ++b) {
+      int c = 0;
+      for (int u = 0; u < 32 && u < nthreads; ++u) c += ((base(u) % 32 + 32) % 32 == b);
+      worst = c > worst ? c : worst;
+    }
+  } else {
+    for (int h = 0; h < 2; ++h)
+      for (int b = 0; b < 16; ++b) {
+        int c = 0;
+        for (int u = 16 * h; u < 16 * h + 16 && u < nthreads; ++u) c += ((base(u) % 16 + 16) % 16 == b);
+        worst = c > worst ? c : worst;
+      }
+  }
+  return worst;
+}
+
+template <int D, typename T>
 struct Cfg {
-  static constexpr int RP = NP + 1;                  // row pitch (odd)
-  static constexpr int PL = NP * RP;                 // plane pitch
-  static constexpr int TSZ = (D == 2) ? NP * RP : NP * PL;
-  static constexpr int NL = (D == 2) ? NP : NP * NP; // lines per direction per patch
-  static constexpr int CELL = (D == 2) ? NC * NC : NC * NC * NC;
-  static constexpr int NCH = 1 << D;                 // cells per patch
+#ifndef IPMG_R32
+#define IPMG_R32 2
+#endif
+  static constexpr int R = sizeof(T) == 4 ? IPMG_R32 : 1;     // lines per thread
+  static constexpr int RP = NP + 1;                           // row pitch (odd)
+  static constexpr int NL = (D == 2) ? NP : NP * NP;          // lines per direction per patch
+  static constexpr int G = NL / R;                            // line groups per patch
+  static constexpr int CELL = ipow(NC, D);
+  static constexpr int NCH = 1 << D;                          // cells per patch
   static constexpr int PATCH = NCH * CELL;
-  static constexpr int NFP = NL;                     // tangential points per face
-  static constexpr int PPC = (256 / NL) > 1 ? (256 / NL) : 1;
-  static constexpr int LINES = PPC * NL;
-  static constexpr int NT0 = ((LINES + 31) / 32) * 32;
-  static constexpr int NT = NT0 > 256 ? 256 : NT0;
+  static constexpr int NFP = NL;                              // tangential points per face
+  static constexpr int NNB = 2 * D * (1 << (D - 1));          // face-neighbour cells per patch
+#ifndef IPMG_GROUPS_TARGET
+#define IPMG_GROUPS_TARGET 32
+#endif
+  static constexpr int PPC = (IPMG_GROUPS_TARGET / G) > 1 ? (IPMG_GROUPS_TARGET / G) : 1;   // patches per CTA
+  static constexpr int GROUPS = PPC * G;
+  static constexpr int NT = (((GROUPS + 31) / 32) * 32) > 256 ? 256 : ((GROUPS + 31) / 32) * 32;
+
+  // line base offset of group g (first line) of patch p for direction a
+  static constexpr int line_base(int a, int p, int g, int pl, int tsz) {
+    return (D == 2) ? (p * tsz + (a == 0 ? g * RP : g))
+                    : (p * tsz + (a == 0 ? (g % NP) * RP + (g / NP) * pl
+                                         : a == 1 ? (g % NP) + (g / NP) * pl : (g % NP) + (g / NP) * RP));
+  }
+  static constexpr int cost(int pl, int tsz) {
+    int c = 0;
+    for (int a = 0; a < D; ++a) {
+      struct B {
+        int a, pl, tsz;
+        constexpr int operator()(int u) const { return line_base(a, u / G, u % G, pl, tsz); }
+      };
+      const int w = bank_cost<T>(B{a, pl, tsz}, GROUPS < NT ? GROUPS : NT);
+      c = c > w ? c : w;
+    }
+    return c;
+  }
+  static constexpr int pick_pl() {
+    if (D == 2) return NP * RP;
+    int best = NP * RP, bc = 1 << 30;
+    for (int pad = 0; pad < 32; ++pad) {
+      const int pl = NP * RP + pad;
+      const int c = cost(pl, NP * pl + 0);
+      if (c < bc) { bc = c; best = pl; }
+    }
+    return best;
+  }
+  static constexpr int PL = pick_pl();                         // plane pitch
+  static constexpr int pick_tsz() {
+    const int base = (D == 2) ? NP * RP : NP * PL;
+    int best = base, bc = 1 << 30;
+    for (int pad = 0; pad < 32; ++pad) {
+      const int c = cost(PL, base + pad);
+      if (c < bc) { bc = c; best = base + pad; }
+    }
+    return best;
+  }
+  static constexpr int TSZ = pick_tsz();                       // patch pitch
+  // face arrays (F): 2D one padded line per array; 3D an NP x NP grid with
+  // odd row pitch FROW, array pitch FARR chosen so that the transform lines of
+  // neighbouring arrays fall into disjoint banks
+  static constexpr int FROW = NP + 1;
+  static constexpr int pick_farr() {
+    if (D == 2) return NP + 1;
+    int best = NP * FROW, bc = 1 << 30;
+    for (int pad = 0; pad < 64; ++pad) {
+      const int fa = NP * FROW + pad;
+      struct B0 { int fa; constexpr int operator()(int u) const { return (u / NP) * fa + (u % NP) * (NP + 1); } };
+      struct B1 { int fa; constexpr int operator()(int u) const { return (u / NP) * fa + (u % NP); } };
+      const int c0 = bank_cost<T>(B0{fa}, 32), c1 = bank_cost<T>(B1{fa}, 32);
+      const int c = c0 > c1 ? c0 : c1;
+      if (c < bc) { bc = c; best = fa; }
+    }
+    return best;
+  }
+  static constexpr int FARR = pick_farr();
+  static constexpr int FSZ = 4 * D * FARR;                     // face scratch per patch
+  // neighbour-cell staging (cp.async prefetch at kernel start): one slot per
+  // face-neighbour cell, slot pitch SP a multiple of 16 bytes with SP/VE odd so
+  // that the 16-byte row reads of neighbouring slots hit different banks
+  static constexpr int VE = 16 / (int)sizeof(T);
+  static constexpr int SP0 = ((CELL + VE - 1) / VE) * VE;
+  static constexpr int SP = ((SP0 / VE) % 2 == 0) ? SP0 + VE : SP0;
+  static constexpr int NBS = PPC * NNB * SP;                   // staging elements per CTA
+#ifdef IPMG_STAGE
+  static constexpr bool STAGE = (size_t)NBS * sizeof(T) <= 48 * 1024;
+#else
+  static constexpr bool STAGE = false;   // measured: the occupancy loss outweighs the prefetch
+#endif
+  static constexpr int CPB = (CELL * (int)sizeof(T)) % 16 == 0 ? 16 : ((CELL * (int)sizeof(T)) % 8 == 0 ? 8 : 4);
 };
 
 template <typename T>
 __device__ __forceinline__ T fma_(T a, T b, T c) { return fma(a, b, c); }
 
+// interior patches (variant 0, the overwhelming majority) take the path with
+// compile-time constant operands; boundary patches the register-indexed one
+#define IPMG_VAR_SPLIT(var, FAST, SLOW) \
+  if ((var) == 0) { FAST; } else { const int v_ = (var); SLOW; }
+// reciprocal of a positive eigenvalue sum: MUFU approximation (fp32: 1 ulp);
+// fp64: approximation refined by two Newton steps (full precision)
+__device__ __forceinline__ float rcp_(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ double rcp_(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
 // ---------------------------------------------------------------- 1D matrices
-// Each functor: get(i, j) entry of the (NOUT x NIN) matrix applied as
-// out[i] = sum_j get(i,j) in[j]; nz(i,j) structural non-zero (compile-time).
+// get(i, j): entry of the (NOUT x NIN) matrix applied as out[i] = sum_j get(i,j) in[j];
+// nz(i,j): structural non-zero.  The products are evaluated as outer products
+// (column j times in[j] into all accumulators -- the order the compiler picks
+// for ILP), so every functor reads a COLUMN of its matrix contiguously.
 template <typename T>
 struct MassP {   // block-diagonal 2-cell patch mass
-  static __device__ __forceinline__ T get(int i, int j) { return tab<T>().M[i % NC][j % NC]; }
+  static __device__ __forceinline__ T get(int i, int j) {   // symmetric; explicit zero off the cell blocks
+    return (i / NC == j / NC) ? tab<T>().M[j % NC][i % NC] : T(0);
+  }
   static __device__ __forceinline__ constexpr bool nz(int i, int j) { return i / NC == j / NC; }
 };
 template <int V, typename T>
 struct LapP {    // patch stiffness + face terms; cross-cell blocks only touch the interior face
-  static __device__ __forceinline__ T get(int i, int j) { return tab<T>().LP[V][i][j]; }
+  static __device__ __forceinline__ T get(int i, int j) { return tab<T>().LP[V][j][i]; }   // symmetric
   static __device__ __forceinline__ constexpr bool nz(int i, int j) {
     return (i / NC == j / NC) || i == NC - 1 || i == NC || j == NC - 1 || j == NC;
   }
@@ -93,12 +224,112 @@ struct EigT {    // S^T: out[m] = sum_i S[i][m] in[i]
 };
 template <int V, typename T>
 struct Eig {     // S: out[i] = sum_m S[i][m] in[m]
-  static __device__ __forceinline__ T get(int i, int m) { return tab<T>().S[V][i][m]; }
+  static __device__ __forceinline__ T get(int i, int m) { return tab<T>().ST[V][m][i]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+// Interior variant: S = [S_even | S_odd] with S_even[np-1-i][m] = S_even[i][m],
+// S_odd[np-1-i][m] = -S_odd[i][m] (reflection symmetry of the interior patch
+// problem, modes ordered by fe1d.cpp).  Half-size products:
+//   S^T v:  even modes <- S_e^T (v_i + v_{np-1-i}),  odd modes <- S_o^T (v_i - v_{np-1-i})
+//   S w:    E = S_e w_e, O = S_o w_o;  out_i = E_i + O_i,  out_{np-1-i} = E_i - O_i   (i < np/2)
+template <typename T>
+struct EvenT {   // (S_e^T)[m][i] = S[0][i][m],      m, i < np/2
+  static __device__ __forceinline__ T get(int m, int i) { return tab<T>().S[0][i][m]; }
   static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
 };
 template <typename T>
+struct OddT {    // (S_o^T)[m][i] = S[0][i][np/2+m]
+  static __device__ __forceinline__ T get(int m, int i) { return tab<T>().S[0][i][NP / 2 + m]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+template <typename T>
+struct EvenB {   // S_e[i][m] = ST[0][m][i]
+  static __device__ __forceinline__ T get(int i, int m) { return tab<T>().ST[0][m][i]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+template <typename T>
+struct OddB {    // S_o[i][m] = ST[0][np/2+m][i]
+  static __device__ __forceinline__ T get(int i, int m) { return tab<T>().ST[0][NP / 2 + m][i]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+template <int NOUT, int NIN, class A, int R, typename T>
+__device__ __forceinline__ void mv(const T (&in)[R][NIN], T (&out)[R][NOUT], const A& mat);
+template <int NOUT, int NIN, class A, int R>
+__device__ __forceinline__ void mv(const float (&in)[R][NIN], float (&out)[R][NOUT], const A& mat);
+
+template <int R, typename T>
+__device__ __forceinline__ void eigT_eo(const T (&in)[R][NP], T (&out)[R][NP]) {
+  constexpr int H = NP / 2;
+  T e[R][H], o[R][H], we[R][H], wo[R][H];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      e[r][i] = in[r][i] + in[r][NP - 1 - i];
+      o[r][i] = in[r][i] - in[r][NP - 1 - i];
+    }
+  mv<H, H, EvenT<T>, R>(e, we, EvenT<T>{});
+  mv<H, H, OddT<T>, R>(o, wo, OddT<T>{});
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      out[r][m] = we[r][m];
+      out[r][H + m] = wo[r][m];
+    }
+}
+template <int R, typename T>
+__device__ __forceinline__ void eig_eo(const T (&in)[R][NP], T (&out)[R][NP]) {
+  constexpr int H = NP / 2;
+  T ie[R][H], io[R][H], E[R][H], O[R][H];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      ie[r][m] = in[r][m];
+      io[r][m] = in[r][H + m];
+    }
+  mv<H, H, EvenB<T>, R>(ie, E, EvenB<T>{});
+  mv<H, H, OddB<T>, R>(io, O, OddB<T>{});
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      out[r][i] = E[r][i] + O[r][i];
+      out[r][NP - 1 - i] = E[r][i] - O[r][i];
+    }
+}
+
+// runtime-variant versions (boundary patches): entries are loaded with a
+// register-indexed constant load instead of a uniform-register operand
+template <typename T>
+struct LapRT {
+  int v;
+  __device__ __forceinline__ T get(int i, int j) const { return tab<T>().LP[v][j][i]; }
+  static __device__ __forceinline__ constexpr bool nz(int i, int j) { return LapP<0, T>::nz(i, j); }
+};
+template <typename T>
+struct EigTRT {
+  int v;
+  __device__ __forceinline__ T get(int m, int i) const { return tab<T>().S[v][i][m]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+template <typename T>
+struct EigRT {
+  int v;
+  __device__ __forceinline__ T get(int i, int m) const { return tab<T>().ST[v][m][i]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+template <typename T>
+struct SMtRT {
+  int v;
+  __device__ __forceinline__ T get(int m, int i) const { return tab<T>().MS[v][i][m]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+
+template <typename T>
 struct Prol {    // P: (NP x NC)
-  static __device__ __forceinline__ T get(int i, int j) { return tab<T>().P[i][j]; }
+  static __device__ __forceinline__ T get(int i, int j) { return tab<T>().PT[j][i]; }
   static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
 };
 template <typename T>
@@ -107,48 +338,132 @@ struct ProlT {   // P^T: (NC x NP)
   static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
 };
 
-template <int NOUT, int NIN, class A, typename T>
-__device__ __forceinline__ void matvec(const T (&in)[NIN], T (&out)[NOUT]) {
+// out[r][i] = sum_j A(i,j) in[r][j] for R lines sharing every matrix entry
+template <int NOUT, int NIN, class A, int R, typename T>
+__device__ __forceinline__ void mv(const T (&in)[R][NIN], T (&out)[R][NOUT], const A& mat = A{}) {
 #pragma unroll
-  for (int i = 0; i < NOUT; ++i) {
-    T acc = T(0);
+  for (int i = 0; i < NOUT; ++i)
 #pragma unroll
-    for (int j = 0; j < NIN; ++j)
-      if (A::nz(i, j)) acc = fma_(A::get(i, j), in[j], acc);
-    out[i] = acc;
+    for (int r = 0; r < R; ++r) out[r][i] = T(0);
+#pragma unroll
+  for (int j = 0; j < NIN; ++j)
+#pragma unroll
+    for (int i = 0; i < NOUT; ++i)
+      if (A::nz(i, j)) {
+        const T a = mat.get(i, j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[r][i] = fma_(a, in[r][j], out[r][i]);
+      }
+}
+// out[r][i] += sum_j A(i,j) in[r][j]
+template <int NOUT, int NIN, class A, int R, typename T>
+__device__ __forceinline__ void mv_acc(const T (&in)[R][NIN], T (&out)[R][NOUT], const A& mat = A{}) {
+#pragma unroll
+  for (int j = 0; j < NIN; ++j)
+#pragma unroll
+    for (int i = 0; i < NOUT; ++i)
+      if (A::nz(i, j)) {
+        const T a = mat.get(i, j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[r][i] = fma_(a, in[r][j], out[r][i]);
+      }
+}
+
+// ---- fp32: packed FFMA2 (fma.rn.f32x2, sm_100).  Outputs are accumulated in
+// pairs (i, i+1) from a column pair of the matrix (one 64-bit uniform-register
+// constant) times a broadcast input: half the FMA instructions of the scalar
+// form -- the smoother is issue-bound, so this is the main fp32 lever.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra, rb, rc, rd;
+  ra = (unsigned long long)__float_as_uint(a.x) | ((unsigned long long)__float_as_uint(a.y) << 32);
+  rb = (unsigned long long)__float_as_uint(b.x) | ((unsigned long long)__float_as_uint(b.y) << 32);
+  rc = (unsigned long long)__float_as_uint(c.x) | ((unsigned long long)__float_as_uint(c.y) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return make_float2(__uint_as_float((unsigned)rd), __uint_as_float((unsigned)(rd >> 32)));
+}
+template <int NOUT, int NIN, class A, int R, bool ACC>
+__device__ __forceinline__ void mv2(const float (&in)[R][NIN], float (&out)[R][NOUT], const A& mat) {
+  constexpr int NPR = NOUT / 2;
+  float2 acc[R][NPR > 0 ? NPR : 1];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int q = 0; q < NPR; ++q) acc[r][q] = ACC ? make_float2(out[r][2 * q], out[r][2 * q + 1]) : make_float2(0.f, 0.f);
+  float tail[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) tail[r] = (ACC && (NOUT & 1)) ? out[r][NOUT - 1] : 0.f;
+#pragma unroll
+  for (int j = 0; j < NIN; ++j) {
+#pragma unroll
+    for (int q = 0; q < NPR; ++q)
+      if (A::nz(2 * q, j) || A::nz(2 * q + 1, j)) {
+        const float2 a = make_float2(mat.get(2 * q, j), mat.get(2 * q + 1, j));
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r][q] = ffma2(a, make_float2(in[r][j], in[r][j]), acc[r][q]);
+      }
+    if ((NOUT & 1) && A::nz(NOUT - 1, j)) {
+      const float a = mat.get(NOUT - 1, j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) tail[r] = fmaf(a, in[r][j], tail[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+#pragma unroll
+    for (int q = 0; q < NPR; ++q) {
+      out[r][2 * q] = acc[r][q].x;
+      out[r][2 * q + 1] = acc[r][q].y;
+    }
+    if (NOUT & 1) out[r][NOUT - 1] = tail[r];
   }
 }
-
-template <int N, typename T>
-__device__ __forceinline__ void load_line(const T* p, int stride, T (&v)[N]) {
-#pragma unroll
-  for (int j = 0; j < N; ++j) v[j] = p[j * stride];
+template <int NOUT, int NIN, class A, int R>
+__device__ __forceinline__ void mv(const float (&in)[R][NIN], float (&out)[R][NOUT], const A& mat = A{}) {
+  mv2<NOUT, NIN, A, R, false>(in, out, mat);
 }
-template <int N, typename T>
-__device__ __forceinline__ void store_line(T* p, int stride, const T (&v)[N]) {
-#pragma unroll
-  for (int j = 0; j < N; ++j) p[j * stride] = v[j];
+template <int NOUT, int NIN, class A, int R>
+__device__ __forceinline__ void mv_acc(const float (&in)[R][NIN], float (&out)[R][NOUT], const A& mat = A{}) {
+  mv2<NOUT, NIN, A, R, true>(in, out, mat);
 }
 
-// line l of direction a in a patch tensor: base offset and stride
-template <int D>
-__device__ __forceinline__ void line_geom(int a, int l, int& base, int& stride) {
-  using C = Cfg<D>;
+template <int N, int R, typename T>
+__device__ __forceinline__ void load_lines(const T* p, int gap, int stride, T (&v)[R][N]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[r][j] = p[r * gap + j * stride];
+}
+template <int N, int R, typename T>
+__device__ __forceinline__ void store_lines(T* p, int gap, int stride, const T (&v)[R][N]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < N; ++j) p[r * gap + j * stride] = v[r][j];
+}
+
+// line geometry: first line of group g in direction a; lines of a group are
+// `gap` apart (line l and l + G), elements `stride` apart
+template <int D, typename T>
+__device__ __forceinline__ void group_geom(int a, int g, int& base, int& gap, int& stride) {
+  using C = Cfg<D, T>;
+  constexpr int G = C::G;
   if (D == 2) {
-    if (a == 0) { base = l * C::RP; stride = 1; }
-    else        { base = l;         stride = C::RP; }
+    if (a == 0) { base = g * C::RP; gap = G * C::RP; stride = 1; }
+    else        { base = g;         gap = G;         stride = C::RP; }
   } else {
-    const int u = l % NP, v = l / NP;
-    if (a == 0)      { base = u * C::RP + v * C::PL; stride = 1; }
-    else if (a == 1) { base = u + v * C::PL;         stride = C::RP; }
-    else             { base = u + v * C::RP;         stride = C::PL; }
+    // line index l = u + NP * v ; l + G with G a multiple of NP/R ...: compute both explicitly
+    const int u = g % NP, v = g / NP;
+    const int l2 = g + G, u2 = l2 % NP, v2 = l2 / NP;
+    if (a == 0)      { base = u * C::RP + v * C::PL; gap = (u2 * C::RP + v2 * C::PL) - base; stride = 1; }
+    else if (a == 1) { base = u + v * C::PL;         gap = (u2 + v2 * C::PL) - base;          stride = C::RP; }
+    else             { base = u + v * C::RP;         gap = (u2 + v2 * C::RP) - base;          stride = C::PL; }
   }
 }
 
 // smem offset of node (local node l of cell q) inside a patch tensor
-template <int D>
+template <int D, typename T>
 __device__ __forceinline__ int node_of_cell(int q, int l) {
-  using C = Cfg<D>;
+  using C = Cfg<D, T>;
   const int l0 = l % NC, l1 = (l / NC) % NC;
   const int i0 = (q & 1) * NC + l0, i1 = ((q >> 1) & 1) * NC + l1;
   if (D == 2) return i0 + i1 * C::RP;
@@ -158,30 +473,14 @@ __device__ __forceinline__ int node_of_cell(int q, int l) {
 }
 
 // ---------------------------------------------------------------- patch indexing
-struct PatchInfo {
-  int c0[3];      // lowest cell coordinates
-  int var[3];     // boundary variant per direction
-  bool valid;
-};
-
 template <int D>
-__device__ __forceinline__ PatchInfo patch_info(const LevelGeom& g, int colour, long long p) {
-  PatchInfo pi;
-  int m[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) m[a] = (a < D) ? (g.n[a] / 2 - ((colour >> a) & 1)) : 1;
-  const long long np = (long long)m[0] * m[1] * m[2];
-  pi.valid = p < np;
-  long long r = pi.valid ? p : 0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const int j = (int)(r % m[a]);
-    r /= m[a];
-    pi.c0[a] = (a < D) ? ((colour >> a) & 1) + 2 * j : 0;
-    pi.var[a] = (a < D) ? ((pi.c0[a] == 0 ? 1 : 0) | (pi.c0[a] + 2 == g.n[a] ? 2 : 0)) : 0;
-  }
-  return pi;
-}
+struct PInfo {
+  long long coff[1 << D];                 // element offset of every patch cell
+  long long nb[2 * D][1 << (D - 1)];      // neighbour cell across face (a, side), -1: none
+  int var[3];                             // boundary variant per direction
+  int valid;
+  int c0[3];
+};
 
 __host__ __device__ inline long long num_patches(const LevelGeom& g, int dim, int colour) {
   long long np = 1;
@@ -189,470 +488,910 @@ __host__ __device__ inline long long num_patches(const LevelGeom& g, int dim, in
   return np;
 }
 
-// global element offset of cell q of patch pi
-template <int D>
-__device__ __forceinline__ long long patch_cell_offset(const LevelGeom& g, const PatchInfo& pi, int q) {
-  using C = Cfg<D>;
-  return cell_offset_cells(g, pi.c0[0] + (q & 1), pi.c0[1] + ((q >> 1) & 1),
-                           D == 3 ? pi.c0[2] + ((q >> 2) & 1) : 0) * (long long)C::CELL;
+// fills PInfo of the CTA's patches; one thread per (patch, item).  The grid is
+// (x-blocks of PPC patches, patch row j1, patch plane j2) of the colour's patch
+// lattice, so patch coordinates need no division.
+template <int D, typename T>
+__device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g, int colour) {
+  using C = Cfg<D, T>;
+  constexpr int ITEMS = 1 + C::NCH + C::NNB;
+  const int m0 = g.n[0] / 2 - (colour & 1);
+  for (int e = threadIdx.x; e < C::PPC * ITEMS; e += blockDim.x) {
+    const int p = e / ITEMS, it = e % ITEMS;
+    const int j0 = blockIdx.x * C::PPC + p;
+    const bool valid = j0 < m0;
+    const int c0x = (colour & 1) + 2 * (valid ? j0 : 0);
+    const int c0y = ((colour >> 1) & 1) + 2 * (int)blockIdx.y;
+    const int c0z = (D == 3) ? ((colour >> 2) & 1) + 2 * (int)blockIdx.z : 0;
+    PInfo<D>& pi = pis[p];
+    if (it == 0) {
+      pi.valid = valid;
+      pi.c0[0] = c0x;
+      pi.c0[1] = c0y;
+      pi.c0[2] = c0z;
+      pi.var[0] = (c0x == 0 ? 1 : 0) | (c0x + 2 == g.n[0] ? 2 : 0);
+      pi.var[1] = (c0y == 0 ? 1 : 0) | (c0y + 2 == g.n[1] ? 2 : 0);
+      pi.var[2] = (D == 3) ? ((c0z == 0 ? 1 : 0) | (c0z + 2 == g.n[2] ? 2 : 0)) : 0;
+    } else if (it <= C::NCH) {
+      const int q = it - 1;
+      pi.coff[q] = cell_offset_cells(g, c0x + (q & 1), c0y + ((q >> 1) & 1), c0z + ((q >> 2) & 1)) * (long long)C::CELL;
+    } else {
+      const int k2 = it - 1 - C::NCH;                 // (a, side, t)
+      constexpr int PER = 1 << (D - 1);
+      const int fs = k2 / PER, t = k2 % PER, a = fs >> 1, s = fs & 1;
+      // neighbour across face (a, s): shift -1 / +2 along a; tangential bits of t
+      const int sa = s == 0 ? -1 : 2;
+      const int tb = t & 1, tcb = (t >> 1) & 1;
+      const int cx = c0x + (a == 0 ? sa : tb);
+      const int cy = c0y + (a == 1 ? sa : (a == 0 ? tb : tcb));
+      const int cz = c0z + (D == 3 ? (a == 2 ? sa : tcb) : 0);
+      const int ca = a == 0 ? cx : (a == 1 ? cy : cz);
+      const bool ex = valid && ca >= 0 && ca < g.n[a];
+      pi.nb[fs][t] = ex ? cell_offset_cells(g, cx, cy, cz) * (long long)C::CELL : -1LL;
+    }
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- cooperative copies
-// X[p] <- scale * src patch cells (src == nullptr -> zeros)
+template <typename T, int V> struct VecT;
+template <> struct VecT<float, 4> { using type = float4; };
+template <> struct VecT<float, 2> { using type = float2; };
+template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<double, 2> { using type = double2; };
+template <> struct VecT<double, 1> { using type = double; };
+
+// Copies between global cell chunks and the padded patch tensor walk the patch
+// in ROW-major order (a warp covers consecutive patch rows; a row is 2 cell-row
+// segments of NC contiguous global values), with a vector width V that divides
+// NC: global accesses are fully used 16-byte sectors and the shared-memory side
+// has at most a 2-way bank conflict.
+template <typename T>
+constexpr int row_vec() {
+  return sizeof(T) == 4 ? (NC % 4 == 0 ? 4 : (NC % 2 == 0 ? 2 : 1)) : (NC % 2 == 0 ? 2 : 1);
+}
+template <typename VT, typename T>
+__device__ __forceinline__ T vget(const VT& v, int i) { return reinterpret_cast<const T*>(&v)[i]; }
+
+// unit u of a patch -> (cell q, local offset l0 in the cell, patch-tensor node)
 template <int D, typename T>
-__device__ __forceinline__ void load_patches(T* X, const T* __restrict__ src, const LevelGeom& g,
-                                             const PatchInfo* pis, int npc, T scale) {
-  using C = Cfg<D>;
-  for (int e = threadIdx.x; e < npc * C::PATCH; e += blockDim.x) {
-    const int p = e / C::PATCH, r = e % C::PATCH, q = r / C::CELL, l = r % C::CELL;
-    T v = T(0);
-    if (src != nullptr && pis[p].valid) v = scale * __ldg(src + patch_cell_offset<D>(g, pis[p], q) + l);
-    X[p * C::TSZ + node_of_cell<D>(q, l)] = v;
+__device__ __forceinline__ void copy_unit(int u, int& q, int& l0, int& node) {
+  using C = Cfg<D, T>;
+  constexpr int V = row_vec<T>();
+  constexpr int CPR = NP / V;                 // chunks per patch row
+  const int h = u % CPR, row = u / CPR;       // row = i1 (2D) or i1 + NP i2 (3D)
+  const int i0 = h * V, i1 = row % NP, i2 = (D == 3) ? row / NP : 0;
+  q = (i0 / NC) + 2 * (i1 / NC) + 4 * (i2 / NC);
+  l0 = (i0 % NC) + NC * (i1 % NC) + NC * NC * (i2 % NC);
+  node = i0 + i1 * C::RP + i2 * C::PL;
+}
+
+// Calls f(p, q, l0, node) for every copy unit of the CTA's patches.  When
+// NT is a multiple of the units per patch (the usual case), a thread keeps one
+// unit of the patch geometry and only walks the patches.
+template <int D, typename T, class Fn>
+__device__ __forceinline__ void for_units(int npc, Fn&& f) {
+  using C = Cfg<D, T>;
+  constexpr int UPP = C::PATCH / row_vec<T>();
+  if (C::NT % UPP == 0) {
+    int q, l0, node;
+    copy_unit<D, T>(threadIdx.x % UPP, q, l0, node);
+#pragma unroll
+    for (int p = threadIdx.x / UPP; p < C::PPC; p += C::NT / UPP)
+      if (p < npc) f(p, q, l0, node);
+  } else {
+    for (int u = threadIdx.x; u < npc * UPP; u += blockDim.x) {
+      int q, l0, node;
+      copy_unit<D, T>(u % UPP, q, l0, node);
+      f(u / UPP, q, l0, node);
+    }
   }
 }
 
-// dst patch cells <- scale * X[p]  (accumulate: dst += scale * X)
-template <int D, bool ACCUM, typename T>
-__device__ __forceinline__ void store_patches(T* __restrict__ dst, const T* X, const LevelGeom& g,
-                                              const PatchInfo* pis, int npc, T scale) {
-  using C = Cfg<D>;
-  for (int e = threadIdx.x; e < npc * C::PATCH; e += blockDim.x) {
-    const int p = e / C::PATCH, r = e % C::PATCH, q = r / C::CELL, l = r % C::CELL;
-    if (!pis[p].valid) continue;
-    T* o = dst + patch_cell_offset<D>(g, pis[p], q) + l;
-    const T v = scale * X[p * C::TSZ + node_of_cell<D>(q, l)];
-    if (ACCUM) *o += v; else *o = v;
-  }
+// X[p] <- scale * src patch cells (src == nullptr -> zeros)
+template <int D, typename T>
+__device__ __forceinline__ void load_patches(T* X, const T* __restrict__ src, const PInfo<D>* pis, int npc, T scale) {
+  using C = Cfg<D, T>;
+  constexpr int V = row_vec<T>();
+  using VT = typename VecT<T, V>::type;
+  for_units<D, T>(npc, [&](int p, int q, int l0, int node) {
+    VT val;
+    if (src != nullptr && pis[p].valid) val = __ldg(reinterpret_cast<const VT*>(src + pis[p].coff[q] + l0));
+    else val = VT{};
+    T* xp = X + p * C::TSZ + node;
+#pragma unroll
+    for (int v = 0; v < V; ++v) xp[v] = scale * vget<VT, T>(val, v);
+  });
+}
+
+// dst patch cells <- scale * X[p]  (MODE 1: dst += scale * X;  MODE 2: dst = bm - scale * X)
+template <int D, int MODE, typename T>
+__device__ __forceinline__ void store_patches(T* __restrict__ dst, const T* X, const PInfo<D>* pis, int npc, T scale,
+                                              const T* __restrict__ bm = nullptr) {
+  using C = Cfg<D, T>;
+  constexpr int V = row_vec<T>();
+  using VT = typename VecT<T, V>::type;
+  for_units<D, T>(npc, [&](int p, int q, int l0, int node) {
+    if (!pis[p].valid) return;
+    const T* xp = X + p * C::TSZ + node;
+    VT val;
+    T* vp = reinterpret_cast<T*>(&val);
+#pragma unroll
+    for (int v = 0; v < V; ++v) vp[v] = scale * xp[v];
+    VT* o = reinterpret_cast<VT*>(dst + pis[p].coff[q] + l0);
+    if (MODE == 1) {            // accumulate
+      VT old = *o;
+#pragma unroll
+      for (int v = 0; v < V; ++v) vp[v] += reinterpret_cast<const T*>(&old)[v];
+    } else if (MODE == 2) {     // bm - scale X
+      VT bb = __ldg(reinterpret_cast<const VT*>(bm + pis[p].coff[q] + l0));
+#pragma unroll
+      for (int v = 0; v < V; ++v) vp[v] = reinterpret_cast<const T*>(&bb)[v] - vp[v];
+    }
+    *o = val;
+  });
 }
 
 // ---------------------------------------------------------------- face terms
-// Coupling of a patch to the cells across its 2d outer faces (the only part of
-// the residual that reads outside the patch; PAPER.md:196-198 domain of
-// dependence).  For the low face in direction a, with neighbour value u and
-// normal derivative u' on the face (unit h, jump read as u- - u+, A1):
-//   (C x_L)_i = M_tan [ delta_{i,0} (-gamma u + u'/2) - phi_i'(0) u / 2 ]   (i in cell 0)
-// and for the high face
-//   (C x_R)_i = M_tan [ delta_{i,np-1} (-gamma u - u'/2) + phi_i'(1) u / 2 ] (i in cell 1).
-// sgn = +1 adds C x_ext (operator), sgn = -1 subtracts it (smoother right side).
-// FU / FD: PPC x 2 sides x NFP scratch.
+// Coupling of a patch to the cells across its 2d outer faces -- the only part
+// of the residual that reads outside the patch (domain of
+// dependence).  With the neighbour's trace u and normal derivative u' on a face
+// of direction a (unit h; jump read as u- - u+, reading A1), the coupling is
+//   C x_ext = sum_{a, side} CF_{side,u}(i_a) (x)_{b != a} M_b  U  +  CF_{side,u'}(i_a) (x)_{b != a} M_b  U'
+// with, on the low face (cell 0 of the patch), CF_u(i) = -phi_i'(0)/2 - gamma delta_{i0},
+// CF_u'(i) = delta_{i0}/2, and on the high face (cell 1) CF_u(i) = phi_i'(1)/2 -
+// gamma delta_{i,np-1}, CF_u'(i) = -delta_{i,np-1}/2.
+// The traces are computed once per patch into F (all faces), transformed along
+// their tangential directions (face_transform) and then injected as rank-one
+// updates with compile-time coefficients CF(i_a) inside the line pass of
+// direction a (no separate face pass, no atomics).
+//
+// F layout per patch: [family a][side s][kind u/u'][NFP], NFP tangential points
+// (first tangential direction fastest).
+template <int D>
+__device__ __forceinline__ int fidx(int p, int a, int s, int kind) {
+  return ((p * D + a) * 2 + s) * 2 + kind;
+}
+
+// position of tangential point t inside a face array
 template <int D, typename T>
-__device__ void face_terms(T* X, T* FU, T* FD, const T* __restrict__ x, const LevelGeom& g,
-                           const PatchInfo* pis, int npc, T sgn) {
-  using C = Cfg<D>;
+__device__ __forceinline__ int fpos(int t) {
+  using C = Cfg<D, T>;
+  return (D == 2) ? t : (t % NP) + (t / NP) * C::FROW;
+}
+
+// ---- neighbour staging: cp.async copies of every face-neighbour cell of the
+// CTA's patches into shared memory, issued right after setup so that the
+// loads overlap the first line passes (consumed only by the last pass).
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int D, typename T>
+__device__ __forceinline__ void stage_neighbors(T* NB, const T* __restrict__ x, const PInfo<D>* pis, int npc) {
+  using C = Cfg<D, T>;
+  constexpr int EPC = C::CPB / (int)sizeof(T);            // elements per copy
+  constexpr int UPC = C::CELL / EPC;                       // copies per cell
+  for (int e = threadIdx.x; e < npc * C::NNB * UPC; e += blockDim.x) {
+    const int slot = e / UPC, c = e % UPC, p = slot / C::NNB, k = slot % C::NNB;
+    const long long nb = pis[p].nb[k >> (D - 1)][k & ((1 << (D - 1)) - 1)];
+    if (nb >= 0) cp_async<C::CPB>(NB + slot * C::SP + c * EPC, x + nb + c * EPC);
+  }
+  cp_async_commit();
+}
+
+// Traces of the neighbour cells: one work unit computes NC face points (the
+// points of one neighbour cell sharing the second tangential index).  It reads
+// the NC cell rows that carry them (row = NC contiguous values; for normal
+// directions x and y the rows form one contiguous slab) -- from the staged copy
+// in shared memory, or from global memory -- and forms u = x(face node) and
+// u' = sum_j phi_j'(face) x_j (unit h).
+// Transform mode of family a along tangential direction b (the direction the
+// family is injected in is a itself, see face_inject): smoother: b < a ->
+// S_b^T M (b already in eigen-space), b > a -> M; operator: b < a -> M (the
+// mass the earlier pass applied to the volume term), b > a -> none.
+// 0 none, 1 mass, 2 S^T M
+template <bool SMOOTHER>
+__host__ __device__ constexpr int face_mode(int a, int b) {
+  return SMOOTHER ? (b < a ? 2 : 1) : (b < a ? 1 : 0);
+}
+__host__ __device__ constexpr int first_tan(int a) { return a == 0 ? 1 : 0; }
+__host__ __device__ constexpr int second_tan(int a) { return a == 2 ? 1 : 2; }
+
+template <typename T>
+struct MassC {   // cell mass (NC x NC)
+  static __device__ __forceinline__ T get(int i, int j) { return tab<T>().M[j][i]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+template <int NOUT, int NIN, class A, int R, typename T>
+__device__ __forceinline__ void mv(const T (&in)[R][NIN], T (&out)[R][NOUT], const A& mat);
+template <int NOUT, int NIN, class A, int R>
+__device__ __forceinline__ void mv(const float (&in)[R][NIN], float (&out)[R][NOUT], const A& mat);
+
+template <int D, int A, bool STAGED, bool SMOOTHER, typename T>
+__device__ __forceinline__ void trace_unit(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>& pi, int p,
+                                           int s, int h, int ic) {
+  using C = Cfg<D, T>;
   const TabData<K, T>& tb = tab<T>();
-#pragma unroll 1
-  for (int a = 0; a < D; ++a) {
-    // (1) traces of the neighbour cells on the two outer faces of direction a
-    const int b = (a == 0) ? 1 : 0;
-    const int c = (a == 2) ? 1 : 2;    // second tangential direction (3D)
-    int strd[3] = {1, NC, NC * NC};
-    for (int e = threadIdx.x; e < npc * 2 * C::NFP; e += blockDim.x) {
-      const int p = e / (2 * C::NFP), s = (e / C::NFP) & 1, t = e % C::NFP;
-      const PatchInfo& pi = pis[p];
-      const bool exists = pi.valid && (s == 0 ? pi.c0[a] > 0 : pi.c0[a] + 2 < g.n[a]);
-      T u = T(0), du = T(0);
-      if (exists) {
-        const int ib = t % NP, ic = t / NP;
-        int cc[3] = {pi.c0[0], pi.c0[1], pi.c0[2]};
-        cc[a] = (s == 0) ? pi.c0[a] - 1 : pi.c0[a] + 2;
-        cc[b] += ib / NC;
-        if (D == 3) cc[c] += ic / NC;
-        const long long base = cell_offset_cells(g, cc[0], cc[1], cc[2]) * C::CELL +
-                               (ib % NC) * strd[b] + (D == 3 ? (ic % NC) * strd[c] : 0);
-        const T* px = x + base;
-        const int sa = strd[a];
-        if (s == 0) {
+  constexpr int V = row_vec<T>();
+  using VT = typename VecT<T, V>::type;
+  const int tc = h + ((D == 3 && ic >= NC) ? 2 : 0);
+  const long long nb = pi.nb[2 * A + s][tc];
+  T u[NC], du[NC];
 #pragma unroll
-          for (int j = 0; j < NC; ++j) du = fma_(tb.d1[j], __ldg(px + j * sa), du);
-          u = __ldg(px + (NC - 1) * sa);
-        } else {
+  for (int i = 0; i < NC; ++i) u[i] = du[i] = T(0);
+  if (nb >= 0) {
+    // rows: A=0 -> row lb = x_{., lb, lc}; A=1 -> row j = x_{., j, lc}; A=2 -> row j = x_{., lc, j}
+    const int lc = ic % NC;
+    const int off = (D == 3 ? (A == 2 ? NC * lc : NC * NC * lc) : 0);
+    const T* base = STAGED ? NB + (p * C::NNB + (2 * A + s) * (1 << (D - 1)) + tc) * C::SP + off : x + nb + off;
+    constexpr int RS = (A == 2) ? NC * NC : NC;       // row stride
+    const int jf = (s == 0) ? NC - 1 : 0;             // face node along the normal
 #pragma unroll
-          for (int j = 0; j < NC; ++j) du = fma_(tb.d0[j], __ldg(px + j * sa), du);
-          u = __ldg(px);
+    for (int rr = 0; rr < NC; ++rr) {
+      T row[NC];
+#pragma unroll
+      for (int c = 0; c < NC / V; ++c) {
+        const VT val = STAGED ? reinterpret_cast<const VT*>(base + rr * RS)[c]
+                              : __ldg(reinterpret_cast<const VT*>(base + rr * RS) + c);
+#pragma unroll
+        for (int v = 0; v < V; ++v) row[c * V + v] = vget<VT, T>(val, v);
+      }
+      if (A == 0) {                                   // row rr is face point lb = rr
+        T acc = T(0);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc = fma_(s == 0 ? tb.d1[j] : tb.d0[j], row[j], acc);
+        du[rr] = acc;
+        u[rr] = (s == 0) ? row[NC - 1] : row[0];
+      } else {                                        // row rr is normal index j = rr
+        const T dj = (s == 0) ? tb.d1[rr] : tb.d0[rr];
+#pragma unroll
+        for (int lb = 0; lb < NC; ++lb) du[lb] = fma_(dj, row[lb], du[lb]);
+        if (rr == jf) {
+#pragma unroll
+          for (int lb = 0; lb < NC; ++lb) u[lb] = row[lb];
         }
       }
-      FU[e] = u;
-      FD[e] = du;
     }
-    __syncthreads();
-    // (2) tangential mass M_tan = M^P (x M^P): line passes over the face grid
-#pragma unroll 1
-    for (int tdim = 0; tdim < D - 1; ++tdim) {
-      const int nlines = npc * 2 * 2 * (D == 3 ? NP : 1);
-      for (int e = threadIdx.x; e < nlines; e += blockDim.x) {
-        const int which = e & 1;                       // 0: FU, 1: FD
-        const int rest = e >> 1;
-        T* arr = which ? FD : FU;
-        int base, stride;
-        if (D == 2) { base = rest * C::NFP; stride = 1; }
-        else {
-          const int ps = rest / NP, o = rest % NP;     // ps = p*2+s
-          if (tdim == 0) { base = ps * C::NFP + o * NP; stride = 1; }
-          else           { base = ps * C::NFP + o;      stride = NP; }
-        }
-        T v[NP], w[NP];
-        load_line<NP>(arr + base, stride, v);
-        matvec<NP, NP, MassP<T>>(v, w);
-        store_line<NP>(arr + base, stride, w);
-      }
-      __syncthreads();
-    }
-    // (3) add the coupling along the lines of direction a
-    for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-      const int p = e / C::NL, l = e % C::NL;
-      int base, stride;
-      line_geom<D>(a, l, base, stride);
-      T* px = X + p * C::TSZ + base;
-      const T ul = FU[(p * 2 + 0) * C::NFP + l], dl = FD[(p * 2 + 0) * C::NFP + l];
-      const T uh = FU[(p * 2 + 1) * C::NFP + l], dh = FD[(p * 2 + 1) * C::NFP + l];
-      const T half = T(0.5);
+  }
+  if (face_mode<SMOOTHER>(A, first_tan(A)) == 1) {
+    // block-diagonal tangential mass along the first tangential direction, in registers
+    T in2[2][NC], out2[2][NC];
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        T lo = -half * tb.d0[i] * ul;
-        if (i == 0) lo += -tb.gamma * ul + half * dl;
-        T hi = half * tb.d1[i] * uh;
-        if (i == NC - 1) hi += -tb.gamma * uh - half * dh;
-        px[i * stride] += sgn * lo;
-        px[(NC + i) * stride] += sgn * hi;
-      }
+    for (int i = 0; i < NC; ++i) {
+      in2[0][i] = u[i];
+      in2[1][i] = du[i];
+    }
+    mv<NC, NC, MassC<T>, 2>(in2, out2, MassC<T>{});
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      u[i] = out2[0][i];
+      du[i] = out2[1][i];
+    }
+  }
+  T* fu = F + fidx<D>(p, A, s, 0) * C::FARR;
+  T* fd = F + fidx<D>(p, A, s, 1) * C::FARR;
+#pragma unroll
+  for (int lb = 0; lb < NC; ++lb) {
+    const int pos = fpos<D, T>(h * NC + lb + NP * ic);
+    fu[pos] = u[lb];
+    fd[pos] = du[lb];
+  }
+}
+
+template <int D, bool STAGED, bool SMOOTHER, typename T>
+__device__ __forceinline__ void face_traces(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis, int npc) {
+  constexpr int NIC = (D == 3) ? NP : 1;
+  constexpr int UPF = 2 * 2 * NIC;                    // units per face family: side x half x ic
+  for (int e = threadIdx.x; e < npc * D * UPF; e += blockDim.x) {
+    const int p = e / (D * UPF), r = e % (D * UPF), a = r / UPF, w = r % UPF;
+    const int s = w & 1, h = (w >> 1) & 1, ic = w >> 2;
+    if (a == 0) trace_unit<D, 0, STAGED, SMOOTHER>(F, x, NB, pis[p], p, s, h, ic);
+    else if (a == 1) trace_unit<D, 1, STAGED, SMOOTHER>(F, x, NB, pis[p], p, s, h, ic);
+    else trace_unit<D, (D == 3 ? 2 : 1), STAGED, SMOOTHER>(F, x, NB, pis[p], p, s, h, ic);
+  }
+}
+
+// traces + tangential transforms of all face families, with the staging wait
+template <int D, bool SMOOTHER, typename T>
+__device__ __forceinline__ void faces_prepare(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis, int npc);
+
+// Tangential transform of the face arrays of family a along tangential
+// direction b (see the mode rule below).
+template <int V, typename T>
+struct SMtM {
+  static __device__ __forceinline__ T get(int m, int i) { return tab<T>().MS[V][i][m]; }
+  static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
+};
+
+// one face-array line (non-inlined so that the loop around it cannot hoist the
+// matrix constants into registers)
+template <typename T>
+__device__ __noinline__ void face_line(T* base, int stride, int mode, int var) {
+  T v[1][NP], w[1][NP];
+  load_lines<NP, 1>(base, 0, stride, v);
+  if (mode == 1) mv<NP, NP, MassP<T>, 1>(v, w);
+  else { IPMG_VAR_SPLIT(var, (mv<NP, NP, SMtM<0, T>, 1>(v, w)), (mv<NP, NP, SMtRT<T>, 1>(v, w, SMtRT<T>{v_}))); }
+  store_lines<NP, 1>(base, 0, stride, w);
+}
+
+template <int D, bool SMOOTHER, typename T>
+__device__ __forceinline__ void face_transform(T* F, const PInfo<D>* pis, int npc) {
+  using C = Cfg<D, T>;
+  // first tangential direction: only the S^T M transforms are left (mass was fused)
+  constexpr bool any1 = SMOOTHER;   // families a >= 1 have first tangential b = 0 < a
+  if (any1) {
+    const int nl = (D == 2) ? 1 : NP;             // lines per array
+#pragma unroll 1
+    for (int e = threadIdx.x; e < npc * D * 4 * nl; e += blockDim.x) {
+      const int o = e % nl, arr = e / nl;         // arr = fidx(p, a, s, kind)
+      const int a = (arr / 4) % D, p = arr / (4 * D);
+      if (face_mode<SMOOTHER>(a, first_tan(a)) != 2) continue;
+      T* base = F + arr * C::FARR + (D == 2 ? 0 : o * C::FROW);
+      face_line<T>(base, 1, 2, pis[p].var[first_tan(a)]);
     }
     __syncthreads();
+  }
+  if (D == 3) {                                   // second tangential direction
+#pragma unroll 1
+    for (int e = threadIdx.x; e < npc * D * 4 * NP; e += blockDim.x) {
+      const int o = e % NP, arr = e / NP;
+      const int a = (arr / 4) % D, p = arr / (4 * D);
+      const int b = second_tan(a);
+      const int mode = face_mode<SMOOTHER>(a, b);
+      if (mode == 0) continue;
+      T* base = F + arr * C::FARR + o;
+      face_line<T>(base, C::FROW, mode, pis[p].var[b]);
+    }
+    __syncthreads();
+  }
+}
+
+template <int D, bool SMOOTHER, typename T>
+__device__ __forceinline__ void faces_prepare(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis,
+                                              int npc) {
+  using C = Cfg<D, T>;
+  if (C::STAGE) {
+    cp_async_wait_all();
+    __syncthreads();
+    face_traces<D, true, SMOOTHER>(F, x, NB, pis, npc);
+  } else {
+    face_traces<D, false, SMOOTHER>(F, x, NB, pis, npc);
+  }
+  __syncthreads();
+  face_transform<D, SMOOTHER>(F, pis, npc);
+}
+
+// y[r][i] += SGN * sum_{side,kind} CF_{side,kind}(i) G_{side,kind}[t(line r)]:
+// the coupling of face family a, added in the line pass of direction a (the
+// line's tangential point is t = line index l)
+template <int D, int SGN, int R, typename T>
+__device__ __forceinline__ void face_inject(T (&y)[R][NP], const T* F, int p, int a, int g) {
+  using C = Cfg<D, T>;
+  const TabData<K, T>& tb = tab<T>();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int pos = fpos<D, T>(g + r * C::G);
+    const T ul = F[fidx<D>(p, a, 0, 0) * C::FARR + pos], dl = F[fidx<D>(p, a, 0, 1) * C::FARR + pos];
+    const T uh = F[fidx<D>(p, a, 1, 0) * C::FARR + pos], dh = F[fidx<D>(p, a, 1, 1) * C::FARR + pos];
+    const T sg = T(SGN);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      T lo = tb.CF[0][i] * ul;
+      if (i == 0) lo = fma_(tb.CF[1][i], dl, lo);
+      y[r][i] = fma_(sg, lo, y[r][i]);
+      T hi = tb.CF[2][NC + i] * uh;
+      if (i == NC - 1) hi = fma_(tb.CF[3][NC + i], dh, hi);
+      y[r][NC + i] = fma_(sg, hi, y[r][NC + i]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- line-pass driver
+// calls f(p, g, base, gap, stride) for the group of R lines of direction a owned
+// by this thread.  Exactly one group per thread (NT >= GROUPS): a loop here
+// would let the compiler hoist the loop-invariant matrix constants out of it
+// into ~NP^2 ordinary registers.
+template <int D, typename T, class Fn>
+__device__ __forceinline__ void for_groups(int a, int npc, Fn&& f) {
+  using C = Cfg<D, T>;
+  static_assert(C::NT >= C::GROUPS, "one line group per thread");
+  const int u = threadIdx.x;
+  if (u < npc * C::G) {
+    const int p = u / C::G, g = u % C::G;
+    int base, gap, stride;
+    group_geom<D, T>(a, g, base, gap, stride);
+    f(p, g, p * C::TSZ + base, gap, stride);
+  }
+}
+
+// ---------------------------------------------------------------- direct global rows
+// The first line pass (x-lines = patch rows) reads its rows straight from
+// global memory and the last x-pass writes them straight back: a patch row is
+// two cell-row segments of NC contiguous values, so these are full-sector
+// vector accesses and no separate global<->shared copy phase is needed.
+// Row l: 2D l = i1; 3D l = i1 + NP i2.
+template <int D>
+__device__ __forceinline__ void row_cells(int l, int& qlo, int& r0) {
+  const int i1 = l % NP, i2 = (D == 3) ? l / NP : 0;
+  qlo = 2 * (i1 / NC) + 4 * (i2 / NC);
+  r0 = NC * (i1 % NC) + NC * NC * (i2 % NC);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void load_seg(const T* __restrict__ src, T scale, T* out) {
+  using VT = typename VecT<T, V>::type;
+#pragma unroll
+  for (int c = 0; c < NC / V; ++c) {
+    const VT val = __ldg(reinterpret_cast<const VT*>(src) + c);
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[c * V + v] = scale * vget<VT, T>(val, v);
+  }
+}
+// MODE 0: dst = scale*v; 1: dst += scale*v; 2: dst = bm - scale*v
+template <int MODE, typename T, int V>
+__device__ __forceinline__ void store_seg(T* __restrict__ dst, const T* __restrict__ bm, T scale, const T* in) {
+  using VT = typename VecT<T, V>::type;
+#pragma unroll
+  for (int c = 0; c < NC / V; ++c) {
+    VT val;
+    T* vp = reinterpret_cast<T*>(&val);
+#pragma unroll
+    for (int v = 0; v < V; ++v) vp[v] = scale * in[c * V + v];
+    VT* o = reinterpret_cast<VT*>(dst) + c;
+    if (MODE == 1) {
+      const VT old = *o;
+#pragma unroll
+      for (int v = 0; v < V; ++v) vp[v] += reinterpret_cast<const T*>(&old)[v];
+    } else if (MODE == 2) {
+      const VT bb = __ldg(reinterpret_cast<const VT*>(bm) + c);
+#pragma unroll
+      for (int v = 0; v < V; ++v) vp[v] = reinterpret_cast<const T*>(&bb)[v] - vp[v];
+    }
+    *o = val;
+  }
+}
+
+// rows g + r G (r < R) of patch pi from global (zeros if src == nullptr / invalid)
+template <int D, int R, typename T>
+__device__ __forceinline__ void load_rows(const T* __restrict__ src, const PInfo<D>& pi, int g, T scale,
+                                          T (&v)[R][NP]) {
+  using C = Cfg<D, T>;
+  constexpr int V = row_vec<T>();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (src != nullptr && pi.valid) {
+      int qlo, r0;
+      row_cells<D>(g + r * C::G, qlo, r0);
+      load_seg<T, V>(src + pi.coff[qlo] + r0, scale, &v[r][0]);
+      load_seg<T, V>(src + pi.coff[qlo + 1] + r0, scale, &v[r][NC]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) v[r][j] = T(0);
+    }
+  }
+}
+template <int D, int MODE, int R, typename T>
+__device__ __forceinline__ void store_rows(T* __restrict__ dst, const T* __restrict__ bm, const PInfo<D>& pi, int g,
+                                           T scale, const T (&v)[R][NP]) {
+  using C = Cfg<D, T>;
+  constexpr int V = row_vec<T>();
+  if (!pi.valid) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int qlo, r0;
+    row_cells<D>(g + r * C::G, qlo, r0);
+    store_seg<MODE, T, V>(dst + pi.coff[qlo] + r0, bm ? bm + pi.coff[qlo] + r0 : nullptr, scale, &v[r][0]);
+    store_seg<MODE, T, V>(dst + pi.coff[qlo + 1] + r0, bm ? bm + pi.coff[qlo + 1] + r0 : nullptr, scale, &v[r][NC]);
+  }
+}
+// lines of the LAST direction (2D: columns i0 = l; 3D: z-lines (i0, i1) = l) straight to global:
+// element j of a line -> cell q(l, j), in-cell offset; per store instruction the
+// warp's consecutive lines are consecutive addresses (coalesced)
+template <int D, int MODE, int R, typename T>
+__device__ __forceinline__ void store_last_lines(T* __restrict__ dst, const T* __restrict__ bm, const PInfo<D>& pi,
+                                                 int g, T scale, const T (&v)[R][NP]) {
+  using C = Cfg<D, T>;
+  if (!pi.valid) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int l = g + r * C::G;
+    const int i0 = l % NP, i1 = (D == 3) ? l / NP : 0;
+    const int qb = (i0 / NC) + (D == 3 ? 2 * (i1 / NC) : 0);           // cell bits of the other directions
+    const int ob = (i0 % NC) + (D == 3 ? NC * (i1 % NC) : 0);
+    constexpr int QS = (D == 2) ? 2 : 4, SS = (D == 2) ? NC : NC * NC;  // cell step / in-cell stride along the line
+    const long long o_lo = pi.coff[qb] + ob, o_hi = pi.coff[qb + QS] + ob;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const long long o = (j < NC ? o_lo : o_hi) + (long long)(j % NC) * SS;
+      T val = scale * v[r][j];
+      if (MODE == 1) val += dst[o];
+      else if (MODE == 2) val = __ldg(bm + o) - val;
+      dst[o] = val;
+    }
   }
 }
 
 // ---------------------------------------------------------------- volume term
-// X <- A_jj(unit) X  (Kronecker sum with the patch matrices)
-// using T1 as scratch:   2D: y = M1 (L0 x) + L1 (M0 x)
-//                        3D: y = M2 (L1 M0 x + M1 L0 x) + L2 (M1 M0 x)
-template <int V, typename T>
-__device__ __forceinline__ void lap_line(const T (&v)[NP], T (&w)[NP]) { matvec<NP, NP, LapP<V, T>>(v, w); }
-
-template <typename T>
-__device__ __forceinline__ void lap_line_v(int var, const T (&v)[NP], T (&w)[NP]) {
-  switch (var) {
-    case 0: lap_line<0>(v, w); break;
-    case 1: lap_line<1>(v, w); break;
-    case 2: lap_line<2>(v, w); break;
-    default: lap_line<3>(v, w); break;
+// y = A_jj(unit) x + C x_ext (Kronecker sum with the patch matrices,
+// PAPER.md:118-126, plus the face coupling injected in the last pass)
+//   2D: y = M1 (L0 x) + L1 (M0 x)                         + C x_ext
+//   3D: y = M2 (L1 M0 x + M1 L0 x) + L2 (M1 M0 x)         + C x_ext
+// vol_pre: all passes but the last (x-rows come in registers); vol_last: the
+// last pass, lines handed to out(p, g, base, gap, stride, y).  X, T1: smem.
+template <int D, bool FACES, typename T>
+__device__ void vol_pre(T (&xr)[Cfg<D, T>::R][NP], T* X, T* T1, const T* F, const PInfo<D>* pis, int npc) {
+  using C = Cfg<D, T>;
+  constexpr int R = C::R;
+  for_groups<D, T>(0, npc, [&](int p, int g, int base, int gap, int stride) {
+    T w[R][NP];
+    mv<NP, NP, MassP<T>, R>(xr, w);
+    store_lines<NP, R>(T1 + base, gap, stride, w);
+    IPMG_VAR_SPLIT(pis[p].var[0], (mv<NP, NP, LapP<0, T>, R>(xr, w)), (mv<NP, NP, LapRT<T>, R>(xr, w, LapRT<T>{v_})));
+    if (FACES) face_inject<D, 1, R>(w, F, p, 0, g);
+    store_lines<NP, R>(X + base, gap, stride, w);
+  });
+  __syncthreads();
+  if (D == 3) {
+    // y-lines: X <- L1 m0 + M1 l0 (+ y-face coupling) ; T1 <- M1 m0
+    for_groups<D, T>(1, npc, [&](int p, int g, int base, int gap, int stride) {
+      T m[R][NP], lx[R][NP], y[R][NP];
+      load_lines<NP, R>(T1 + base, gap, stride, m);
+      load_lines<NP, R>(X + base, gap, stride, lx);
+      mv<NP, NP, MassP<T>, R>(lx, y);
+      IPMG_VAR_SPLIT(pis[p].var[1], (mv_acc<NP, NP, LapP<0, T>, R>(m, y)), (mv_acc<NP, NP, LapRT<T>, R>(m, y, LapRT<T>{v_})));
+      if (FACES) face_inject<D, 1, R>(y, F, p, 1, g);
+      store_lines<NP, R>(X + base, gap, stride, y);
+      mv<NP, NP, MassP<T>, R>(m, y);
+      store_lines<NP, R>(T1 + base, gap, stride, y);
+    });
+    __syncthreads();
   }
 }
-
-template <int D, typename T>
-__device__ void volume_apply(T* X, T* T1, const PatchInfo* pis, int npc) {
-  using C = Cfg<D>;
-  // pass over x-lines: T1 = M0 x, X = L0 x
-  for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-    const int p = e / C::NL, l = e % C::NL;
-    int base, stride;
-    line_geom<D>(0, l, base, stride);
-    T v[NP], m[NP], w[NP];
-    load_line<NP>(X + p * C::TSZ + base, stride, v);
-    matvec<NP, NP, MassP<T>>(v, m);
-    lap_line_v(pis[p].var[0], v, w);
-    store_line<NP>(T1 + p * C::TSZ + base, stride, m);
-    store_line<NP>(X + p * C::TSZ + base, stride, w);
-  }
-  __syncthreads();
-  if (D == 2) {
-    for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-      const int p = e / C::NL, l = e % C::NL;
-      int base, stride;
-      line_geom<D>(1, l, base, stride);
-      T m[NP], lx[NP], y[NP], t[NP];
-      load_line<NP>(T1 + p * C::TSZ + base, stride, m);
-      load_line<NP>(X + p * C::TSZ + base, stride, lx);
-      matvec<NP, NP, MassP<T>>(lx, y);
-      lap_line_v(pis[p].var[1], m, t);
-#pragma unroll
-      for (int i = 0; i < NP; ++i) y[i] += t[i];
-      store_line<NP>(X + p * C::TSZ + base, stride, y);
-    }
-    __syncthreads();
-  } else {
-    // y-lines: X <- L1 m0 + M1 l0 ; T1 <- M1 m0
-    for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-      const int p = e / C::NL, l = e % C::NL;
-      int base, stride;
-      line_geom<D>(1, l, base, stride);
-      T m[NP], lx[NP], y[NP], t[NP];
-      load_line<NP>(T1 + p * C::TSZ + base, stride, m);
-      load_line<NP>(X + p * C::TSZ + base, stride, lx);
-      matvec<NP, NP, MassP<T>>(lx, y);
-      lap_line_v(pis[p].var[1], m, t);
-#pragma unroll
-      for (int i = 0; i < NP; ++i) y[i] += t[i];
-      store_line<NP>(X + p * C::TSZ + base, stride, y);
-      matvec<NP, NP, MassP<T>>(m, t);
-      store_line<NP>(T1 + p * C::TSZ + base, stride, t);
-    }
-    __syncthreads();
-    // z-lines: X <- M2 X + L2 T1
-    for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-      const int p = e / C::NL, l = e % C::NL;
-      int base, stride;
-      line_geom<D>(2, l, base, stride);
-      T a[NP], bb[NP], y[NP], t[NP];
-      load_line<NP>(X + p * C::TSZ + base, stride, a);
-      load_line<NP>(T1 + p * C::TSZ + base, stride, bb);
-      matvec<NP, NP, MassP<T>>(a, y);
-      lap_line_v(pis[p].var[2], bb, t);
-#pragma unroll
-      for (int i = 0; i < NP; ++i) y[i] += t[i];
-      store_line<NP>(X + p * C::TSZ + base, stride, y);
-    }
-    __syncthreads();
-  }
+template <int D, bool FACES, typename T, class Out>
+__device__ void vol_last(T* X, T* T1, const T* F, const PInfo<D>* pis, int npc, Out&& out) {
+  using C = Cfg<D, T>;
+  constexpr int R = C::R;
+  constexpr int LAST = D - 1;
+  for_groups<D, T>(LAST, npc, [&](int p, int g, int base, int gap, int stride) {
+    T a[R][NP], bb[R][NP], y[R][NP];
+    load_lines<NP, R>(X + base, gap, stride, a);
+    load_lines<NP, R>(T1 + base, gap, stride, bb);
+    mv<NP, NP, MassP<T>, R>(a, y);
+    IPMG_VAR_SPLIT(pis[p].var[LAST], (mv_acc<NP, NP, LapP<0, T>, R>(bb, y)),
+                   (mv_acc<NP, NP, LapRT<T>, R>(bb, y, LapRT<T>{v_})));
+    if (FACES) face_inject<D, 1, R>(y, F, p, LAST, g);
+    out(p, g, base, gap, stride, y);
+  });
 }
 
 // ---------------------------------------------------------------- fast diagonalisation
-// X <- A_jj(unit)^{-1} X = (x S_a) (sum_a Lambda_a)^{-1} (x S_a^T) X
-// (eq. inverse2d / inverse3d / fast_inverse)
-template <int V, typename T>
-__device__ __forceinline__ void eigT_line(const T (&v)[NP], T (&w)[NP]) { matvec<NP, NP, EigT<V, T>>(v, w); }
-template <int V, typename T>
-__device__ __forceinline__ void eig_line(const T (&v)[NP], T (&w)[NP]) { matvec<NP, NP, Eig<V, T>>(v, w); }
-
-template <typename T>
-__device__ __forceinline__ void eigT_line_v(int var, const T (&v)[NP], T (&w)[NP]) {
-  switch (var) {
-    case 0: eigT_line<0>(v, w); break;
-    case 1: eigT_line<1>(v, w); break;
-    case 2: eigT_line<2>(v, w); break;
-    default: eigT_line<3>(v, w); break;
-  }
+// x = A_jj(unit)^{-1} (rhs - C x_ext) = (x S_a) (sum_a Lambda_a)^{-1} (x S_a^T) (rhs - C x_ext)
+// (eq. inverse2d / inverse3d / fast_inverse).  The face
+// coupling of face family a is subtracted in the forward pass of direction a,
+// with the face arrays transformed into the matching (eigen-)space.
+template <int R, typename T>
+__device__ __forceinline__ void fwd_line(const T (&v)[R][NP], T (&w)[R][NP], int var) {
+  IPMG_VAR_SPLIT(var, (eigT_eo<R>(v, w)), (mv<NP, NP, EigTRT<T>, R>(v, w, EigTRT<T>{v_})));
 }
-template <typename T>
-__device__ __forceinline__ void eig_line_v(int var, const T (&v)[NP], T (&w)[NP]) {
-  switch (var) {
-    case 0: eig_line<0>(v, w); break;
-    case 1: eig_line<1>(v, w); break;
-    case 2: eig_line<2>(v, w); break;
-    default: eig_line<3>(v, w); break;
-  }
+template <int R, typename T>
+__device__ __forceinline__ void bwd_line(const T (&v)[R][NP], T (&w)[R][NP], int var) {
+  IPMG_VAR_SPLIT(var, (eig_eo<R>(v, w)), (mv<NP, NP, EigRT<T>, R>(v, w, EigRT<T>{v_})));
 }
 
-template <int D, bool FORWARD, typename T>
-__device__ __forceinline__ void eig_pass(T* X, int a, const PatchInfo* pis, int npc) {
-  using C = Cfg<D>;
-  for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-    const int p = e / C::NL, l = e % C::NL;
-    int base, stride;
-    line_geom<D>(a, l, base, stride);
-    T v[NP], w[NP];
-    load_line<NP>(X + p * C::TSZ + base, stride, v);
-    if (FORWARD) eigT_line_v(pis[p].var[a], v, w);
-    else eig_line_v(pis[p].var[a], v, w);
-    store_line<NP>(X + p * C::TSZ + base, stride, w);
-  }
-  __syncthreads();
-}
-
-template <int D, typename T>
-__device__ void fast_diag(T* X, const PatchInfo* pis, int npc) {
-  using C = Cfg<D>;
+// S^T, scale by 1/(lsum + lambda_m), S on R lines of the last direction (variant V)
+template <int V, int R, typename T>
+__device__ __forceinline__ void fd_last(T (&v)[R][NP], T (&w)[R][NP], const T (&lsum)[R]) {
+  static_assert(V == 0, "fast path is the interior variant");
   const TabData<K, T>& tb = tab<T>();
-  constexpr int LAST = D - 1;
-#pragma unroll 1
-  for (int a = 0; a < LAST; ++a) eig_pass<D, true>(X, a, pis, npc);
-  // last direction: S^T, divide by the eigenvalue sums, S -- in registers
-  for (int e = threadIdx.x; e < npc * C::NL; e += blockDim.x) {
-    const int p = e / C::NL, l = e % C::NL;
-    int base, stride;
-    line_geom<D>(LAST, l, base, stride);
-    const PatchInfo& pi = pis[p];
-    T lsum = tb.lam[pi.var[0]][l % NP];
-    if (D == 3) lsum += tb.lam[pi.var[1]][l / NP];
-    T v[NP], w[NP];
-    load_line<NP>(X + p * C::TSZ + base, stride, v);
-    eigT_line_v(pi.var[LAST], v, w);
+  eigT_eo<R>(v, w);
 #pragma unroll
-    for (int m = 0; m < NP; ++m) w[m] = w[m] / (lsum + tb.lam[pi.var[LAST]][m]);
-    eig_line_v(pi.var[LAST], w, v);
-    store_line<NP>(X + p * C::TSZ + base, stride, v);
-  }
+  for (int m = 0; m < NP; ++m)
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r][m] *= rcp_(lsum[r] + tb.lam[0][m]);
+  eig_eo<R>(w, v);
+}
+template <int R, typename T>
+__device__ __forceinline__ void fd_last_rt(T (&v)[R][NP], T (&w)[R][NP], const T (&lsum)[R], int var) {
+  const TabData<K, T>& tb = tab<T>();
+  mv<NP, NP, EigTRT<T>, R>(v, w, EigTRT<T>{var});
+#pragma unroll
+  for (int m = 0; m < NP; ++m)
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r][m] *= rcp_(lsum[r] + tb.lam[var][m]);
+  mv<NP, NP, EigRT<T>, R>(w, v, EigRT<T>{var});
+}
+
+// forward passes of all directions but the last (x-rows from registers);
+// face family a is subtracted before the S_a^T of its own pass
+template <int D, bool FACES, typename T>
+__device__ void fd_pre(T (&xr)[Cfg<D, T>::R][NP], T* X, const T* F, const PInfo<D>* pis, int npc) {
+  using C = Cfg<D, T>;
+  constexpr int R = C::R;
+  for_groups<D, T>(0, npc, [&](int p, int g, int base, int gap, int stride) {
+    T w[R][NP];
+    if (FACES) face_inject<D, -1, R>(xr, F, p, 0, g);
+    fwd_line<R>(xr, w, pis[p].var[0]);
+    store_lines<NP, R>(X + base, gap, stride, w);
+  });
   __syncthreads();
-#pragma unroll 1
-  for (int a = LAST - 1; a >= 0; --a) eig_pass<D, false>(X, a, pis, npc);
+  if (D == 3) {
+    for_groups<D, T>(1, npc, [&](int p, int g, int base, int gap, int stride) {
+      T v[R][NP], w[R][NP];
+      load_lines<NP, R>(X + base, gap, stride, v);
+      if (FACES) face_inject<D, -1, R>(v, F, p, 1, g);
+      fwd_line<R>(v, w, pis[p].var[1]);
+      store_lines<NP, R>(X + base, gap, stride, w);
+    });
+    __syncthreads();
+  }
+}
+// last direction (faces, S^T, eigenvalue division, S), then the backward
+// passes; the x-rows of the result are handed to out(p, g, rows)
+template <int D, bool FACES, typename T, class Out>
+__device__ void fd_post(T* X, const T* F, const PInfo<D>* pis, int npc, Out&& out) {
+  using C = Cfg<D, T>;
+  constexpr int R = C::R;
+  constexpr int LAST = D - 1;
+  const TabData<K, T>& tb = tab<T>();
+  for_groups<D, T>(LAST, npc, [&](int p, int g, int base, int gap, int stride) {
+    const PInfo<D>& pi = pis[p];
+    T lsum[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int l = g + r * C::G;           // line id: (m0) in 2D, (m0 + NP m1) in 3D
+      lsum[r] = tb.lam[pi.var[0]][l % NP];
+      if (D == 3) lsum[r] += tb.lam[pi.var[1]][l / NP];
+    }
+    T v[R][NP], w[R][NP];
+    load_lines<NP, R>(X + base, gap, stride, v);
+    if (FACES) face_inject<D, -1, R>(v, F, p, LAST, g);
+    IPMG_VAR_SPLIT(pi.var[LAST], (fd_last<0, R>(v, w, lsum)), (fd_last_rt<R>(v, w, lsum, v_)));
+    store_lines<NP, R>(X + base, gap, stride, v);
+  });
+  __syncthreads();
+  if (D == 3) {
+    for_groups<D, T>(1, npc, [&](int p, int, int base, int gap, int stride) {
+      T v[R][NP], w[R][NP];
+      load_lines<NP, R>(X + base, gap, stride, v);
+      bwd_line<R>(v, w, pis[p].var[1]);
+      store_lines<NP, R>(X + base, gap, stride, w);
+    });
+    __syncthreads();
+  }
+  for_groups<D, T>(0, npc, [&](int p, int g, int base, int gap, int stride) {
+    T v[R][NP], w[R][NP];
+    load_lines<NP, R>(X + base, gap, stride, v);
+    bwd_line<R>(v, w, pis[p].var[0]);
+    out(p, g, w);
+  });
 }
 
 // ---------------------------------------------------------------- kernels
+// rows of this thread's line group (x-pass) loaded from global into registers
 template <int D, typename T>
-__device__ __forceinline__ void setup_patches(PatchInfo* pis, const LevelGeom& g, int colour, long long patch0, int npc) {
-  if (threadIdx.x < npc) pis[threadIdx.x] = patch_info<D>(g, colour, patch0 + threadIdx.x);
-  __syncthreads();
+__device__ __forceinline__ void my_rows(const T* __restrict__ src, const PInfo<D>* pis, int npc, T scale,
+                                        T (&v)[Cfg<D, T>::R][NP]) {
+  using C = Cfg<D, T>;
+  const int u = threadIdx.x;
+  if (u < npc * C::G) load_rows<D, C::R>(src, pis[u / C::G], u % C::G, scale, v);
 }
 
 // y = hs * A x   or, with bminus != nullptr, y = bminus - hs * A x
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D>::NT) vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                           const T* __restrict__ bminus, LevelGeom g) {
-  using C = Cfg<D>;
+__global__ void __launch_bounds__(Cfg<D, T>::NT) vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                              const T* __restrict__ bminus, LevelGeom g) {
+  using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* T1 = X + C::PPC * C::TSZ;
-  T* FU = T1 + C::PPC * C::TSZ;
-  T* FD = FU + C::PPC * 2 * C::NFP;
-  __shared__ PatchInfo pis[C::PPC];
-  const long long patch0 = (long long)blockIdx.x * C::PPC;
-  setup_patches<D, T>(pis, g, 0, patch0, C::PPC);
-  load_patches<D>(X, x, g, pis, C::PPC, T(1));
-  __syncthreads();
-  volume_apply<D>(X, T1, pis, C::PPC);
-  face_terms<D>(X, FU, FD, x, g, pis, C::PPC, T(1));
+  T* F = T1 + C::PPC * C::TSZ;   // PPC * FSZ face scratch
+  T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
+  __shared__ PInfo<D> pis[C::PPC];
+  setup_patches<D, T>(pis, g, 0);
+  if (C::STAGE) stage_neighbors<D>(NB, x, pis, C::PPC);
+  T xr[C::R][NP];
+#ifdef IPMG_ROWS_EARLY
+  my_rows<D>(x, pis, C::PPC, T(1), xr);        // in flight while the traces load
+#endif
+  faces_prepare<D, false>(F, x, NB, pis, C::PPC);
+#ifndef IPMG_ROWS_EARLY
+  my_rows<D>(x, pis, C::PPC, T(1), xr);
+#endif
+  vol_pre<D, true>(xr, X, T1, F, pis, C::PPC);
   const T hs = T(g.hs);
-  if (bminus == nullptr) {
-    store_patches<D, false>(y, X, g, pis, C::PPC, hs);
-  } else {
-    for (int e = threadIdx.x; e < C::PPC * C::PATCH; e += blockDim.x) {
-      const int p = e / C::PATCH, r = e % C::PATCH, q = r / C::CELL, l = r % C::CELL;
-      if (!pis[p].valid) continue;
-      const long long o = patch_cell_offset<D>(g, pis[p], q) + l;
-      y[o] = __ldg(bminus + o) - hs * X[p * C::TSZ + node_of_cell<D>(q, l)];
-    }
-  }
+  if (bminus == nullptr)
+    vol_last<D, true>(X, T1, F, pis, C::PPC, [&](int p, int gg, int, int, int, const T (&yy)[C::R][NP]) {
+      store_last_lines<D, 0, C::R>(y, (const T*)nullptr, pis[p], gg, hs, yy);
+    });
+  else
+    vol_last<D, true>(X, T1, F, pis, C::PPC, [&](int p, int gg, int, int, int, const T (&yy)[C::R][NP]) {
+      store_last_lines<D, 2, C::R>(y, bminus, pis[p], gg, hs, yy);
+    });
 }
 
 // one colour of the multiplicative full-kernel smoother (replacement form):
 // x_out_j = A_jj^{-1} (b_j - C_j x_in) for every patch j of the colour;
 // extra CTAs copy the cells the colour does not cover.
+// cells a shifted colour does not cover (boundary layers c_a in {0, n_a-1} of
+// every shifted direction a) are copied x_out = x_in (zero if x_in == nullptr)
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D>::NT) smooth_kernel(const T* __restrict__ x_in, const T* __restrict__ b,
-                                                            T* __restrict__ x_out, LevelGeom g, int colour,
-                                                            int n_patch_ctas) {
-  using C = Cfg<D>;
-  if ((int)blockIdx.x >= n_patch_ctas) {
-    // copy role: boundary layers c_a in {0, n_a-1} of every shifted direction a
-    long long idx = (long long)(blockIdx.x - n_patch_ctas) * blockDim.x + threadIdx.x;
-    const long long stride_all = (long long)(gridDim.x - n_patch_ctas) * blockDim.x;
-    for (int a = 0; a < D; ++a) {
-      if (!((colour >> a) & 1)) continue;
-      long long layer = 1;
-      for (int bb = 0; bb < D; ++bb) if (bb != a) layer *= g.n[bb];
-      const long long total = 2 * layer * C::CELL;
-      for (long long e = idx; e < total; e += stride_all) {
-        const long long cell = e / C::CELL;
-        const int l = (int)(e % C::CELL);
-        const int side = (int)(cell / layer);
-        long long rem = cell % layer;
-        int cc[3] = {0, 0, 0};
-        for (int bb = 0; bb < D; ++bb) {
-          if (bb == a) continue;
-          cc[bb] = (int)(rem % g.n[bb]);
-          rem /= g.n[bb];
-        }
-        cc[a] = side ? g.n[a] - 1 : 0;
-        const long long o = cell_offset_cells(g, cc[0], cc[1], cc[2]) * C::CELL + l;
-        x_out[o] = x_in ? __ldg(x_in + o) : T(0);
+__global__ void copy_uncovered_kernel(const T* __restrict__ x_in, T* __restrict__ x_out, LevelGeom g, int colour) {
+  using C = Cfg<D, T>;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride_all = (long long)gridDim.x * blockDim.x;
+  for (int a = 0; a < D; ++a) {
+    if (!((colour >> a) & 1)) continue;
+    long long layer = 1;
+    for (int bb = 0; bb < D; ++bb) if (bb != a) layer *= g.n[bb];
+    const long long total = 2 * layer * C::CELL;
+    for (long long e = idx; e < total; e += stride_all) {
+      const long long cell = e / C::CELL;
+      const int l = (int)(e % C::CELL);
+      const int side = (int)(cell / layer);
+      long long rem = cell % layer;
+      int cc[3] = {0, 0, 0};
+      for (int bb = 0; bb < D; ++bb) {
+        if (bb == a) continue;
+        cc[bb] = (int)(rem % g.n[bb]);
+        rem /= g.n[bb];
       }
+      cc[a] = side ? g.n[a] - 1 : 0;
+      const long long o = cell_offset_cells(g, cc[0], cc[1], cc[2]) * C::CELL + l;
+      x_out[o] = x_in ? __ldg(x_in + o) : T(0);
     }
-    return;
   }
+}
+
+// one colour of the multiplicative full-kernel smoother (replacement form):
+// x_out_j = A_jj^{-1} (b_j - C_j x_in) for every patch j of the colour
+template <int D, typename T>
+__global__ void __launch_bounds__(Cfg<D, T>::NT) smooth_kernel(const T* __restrict__ x_in, const T* __restrict__ b,
+                                                               T* __restrict__ x_out, LevelGeom g, int colour) {
+  using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
-  T* FU = X + C::PPC * C::TSZ;
-  T* FD = FU + C::PPC * 2 * C::NFP;
-  __shared__ PatchInfo pis[C::PPC];
-  const long long patch0 = (long long)blockIdx.x * C::PPC;
-  setup_patches<D, T>(pis, g, colour, patch0, C::PPC);
-  load_patches<D>(X, b, g, pis, C::PPC, T(g.hinv));
-  __syncthreads();
-  if (x_in != nullptr) face_terms<D>(X, FU, FD, x_in, g, pis, C::PPC, T(-1));
-  fast_diag<D>(X, pis, C::PPC);
-  store_patches<D, false>(x_out, X, g, pis, C::PPC, T(1));
+  T* F = X + C::PPC * C::TSZ;
+  T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
+  __shared__ PInfo<D> pis[C::PPC];
+  setup_patches<D, T>(pis, g, colour);
+  if (x_in != nullptr && C::STAGE) stage_neighbors<D>(NB, x_in, pis, C::PPC);   // lands during fd_pre
+  T br[C::R][NP];
+#ifdef IPMG_ROWS_EARLY
+  my_rows<D>(b, pis, C::PPC, T(g.hinv), br);    // in flight while the traces load
+#endif
+  auto out = [&](int p, int gg, const T (&w)[C::R][NP]) {
+    store_rows<D, 0, C::R>(x_out, (const T*)nullptr, pis[p], gg, T(1), w);
+  };
+  if (x_in != nullptr) {
+    faces_prepare<D, true>(F, x_in, NB, pis, C::PPC);
+#ifndef IPMG_ROWS_EARLY   // measured: loading the rows after the traces keeps registers low
+    my_rows<D>(b, pis, C::PPC, T(g.hinv), br);
+#endif
+    fd_pre<D, true>(br, X, F, pis, C::PPC);
+    fd_post<D, true>(X, F, pis, C::PPC, out);
+  } else {
+#ifndef IPMG_ROWS_EARLY
+    my_rows<D>(b, pis, C::PPC, T(g.hinv), br);
+#endif
+    fd_pre<D, false>(br, X, F, pis, C::PPC);
+    fd_post<D, false>(X, F, pis, C::PPC, out);
+  }
 }
 
 // additive Schwarz over one colour: x_j += omega A_jj^{-1} r_j
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D>::NT) additive_kernel(const T* __restrict__ r, T* __restrict__ x,
-                                                              LevelGeom g, int colour, T omega) {
-  using C = Cfg<D>;
+__global__ void __launch_bounds__(Cfg<D, T>::NT) additive_kernel(const T* __restrict__ r, T* __restrict__ x,
+                                                                 LevelGeom g, int colour, T omega) {
+  using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
-  __shared__ PatchInfo pis[C::PPC];
-  const long long patch0 = (long long)blockIdx.x * C::PPC;
-  setup_patches<D, T>(pis, g, colour, patch0, C::PPC);
-  load_patches<D>(X, r, g, pis, C::PPC, T(g.hinv));
-  __syncthreads();
-  fast_diag<D>(X, pis, C::PPC);
-  store_patches<D, true>(x, X, g, pis, C::PPC, omega);
+  __shared__ PInfo<D> pis[C::PPC];
+  setup_patches<D, T>(pis, g, colour);
+  T rr[C::R][NP];
+  my_rows<D>(r, pis, C::PPC, T(g.hinv), rr);
+  fd_pre<D, false>(rr, X, X, pis, C::PPC);
+  fd_post<D, false>(X, X, pis, C::PPC, [&](int p, int gg, const T (&w)[C::R][NP]) {
+    store_rows<D, 1, C::R>(x, (const T*)nullptr, pis[p], gg, omega, w);
+  });
+}
+
+template <typename T>
+__device__ __noinline__ void restrict_line(T* base, int stride) {
+  T v[1][NP], w[1][NC];
+  load_lines<NP, 1>(base, 0, stride, v);
+  mv<NC, NP, ProlT<T>, 1>(v, w);
+  store_lines<NC, 1>(base, 0, stride, w);
+}
+template <typename T>
+__device__ __noinline__ void prolong_line(T* base, int stride) {
+  T v[1][NC], w[1][NP];
+  load_lines<NC, 1>(base, 0, stride, v);
+  mv<NP, NC, Prol<T>, 1>(v, w);
+  store_lines<NP, 1>(base, 0, stride, w);
 }
 
 // r_c = P^T (b - hs A x) per parent cell (colour-0 patch); x == nullptr -> P^T b
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D>::NT) restrict_kernel(const T* __restrict__ x, const T* __restrict__ b,
-                                                              T* __restrict__ rc, LevelGeom gf, LevelGeom gc) {
-  using C = Cfg<D>;
+__global__ void __launch_bounds__(Cfg<D, T>::NT) restrict_kernel(const T* __restrict__ x, const T* __restrict__ b,
+                                                                 T* __restrict__ rc, LevelGeom gf, LevelGeom gc) {
+  using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* T1 = X + C::PPC * C::TSZ;
-  T* FU = T1 + C::PPC * C::TSZ;
-  T* FD = FU + C::PPC * 2 * C::NFP;
-  __shared__ PatchInfo pis[C::PPC];
-  const long long patch0 = (long long)blockIdx.x * C::PPC;
-  setup_patches<D, T>(pis, gf, 0, patch0, C::PPC);
+  T* F = T1 + C::PPC * C::TSZ;   // PPC * FSZ face scratch
+  T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
+  __shared__ PInfo<D> pis[C::PPC];
+  setup_patches<D, T>(pis, gf, 0);
   const T hs = T(gf.hs);
   if (x != nullptr) {
-    load_patches<D>(X, x, gf, pis, C::PPC, T(1));
+    if (C::STAGE) stage_neighbors<D>(NB, x, pis, C::PPC);
+    T xr[C::R][NP];
+    my_rows<D>(x, pis, C::PPC, T(1), xr);
+    faces_prepare<D, false>(F, x, NB, pis, C::PPC);
+    vol_pre<D, true>(xr, X, T1, F, pis, C::PPC);
+    vol_last<D, true>(X, T1, F, pis, C::PPC, [&](int, int, int base, int gap, int stride, const T (&yy)[C::R][NP]) {
+      store_lines<NP, C::R>(X + base, gap, stride, yy);
+    });
     __syncthreads();
-    volume_apply<D>(X, T1, pis, C::PPC);
-    face_terms<D>(X, FU, FD, x, gf, pis, C::PPC, T(1));
-    for (int e = threadIdx.x; e < C::PPC * C::PATCH; e += blockDim.x) {
-      const int p = e / C::PATCH, r = e % C::PATCH, q = r / C::CELL, l = r % C::CELL;
-      const int node = p * C::TSZ + node_of_cell<D>(q, l);
-      T bv = T(0);
-      if (pis[p].valid) bv = __ldg(b + patch_cell_offset<D>(gf, pis[p], q) + l);
-      X[node] = bv - hs * X[node];
-    }
+    // T1 <- b ; X <- T1 - hs X
+    load_patches<D>(T1, b, pis, C::PPC, T(1));
+    __syncthreads();
+    for (int e = threadIdx.x; e < C::PPC * C::TSZ; e += blockDim.x) X[e] = T1[e] - hs * X[e];
   } else {
-    load_patches<D>(X, b, gf, pis, C::PPC, T(1));
+    load_patches<D>(X, b, pis, C::PPC, T(1));
   }
   __syncthreads();
-  // P^T along x (all NL lines), then y (lines with i0 < NC), then z (i0,i1 < NC)
+  // P^T along x (all lines), then y (lines with i0 < NC), then z (i0, i1 < NC)
 #pragma unroll 1
   for (int a = 0; a < D; ++a) {
     const int nl = (D == 2) ? (a == 0 ? NP : NC) : (a == 0 ? NP * NP : (a == 1 ? NC * NP : NC * NC));
     for (int e = threadIdx.x; e < C::PPC * nl; e += blockDim.x) {
       const int p = e / nl, li = e % nl;
-      int l;   // line id in line_geom numbering
-      if (D == 2) l = li;
-      else if (a == 0) l = li;                          // (i1, i2) all
-      else if (a == 1) l = (li % NC) + NP * (li / NC);  // (i0 < NC, i2)
-      else l = (li % NC) + NP * (li / NC);              // (i0 < NC, i1 < NC)
+      const int l = (D == 2 || a == 0) ? li : (li % NC) + NP * (li / NC);
       int base, stride;
-      line_geom<D>(a, l, base, stride);
-      T v[NP], w[NC];
-      load_line<NP>(X + p * C::TSZ + base, stride, v);
-      matvec<NC, NP, ProlT<T>>(v, w);
-      store_line<NC>(X + p * C::TSZ + base, stride, w);
+      if (D == 2) { base = a == 0 ? l * C::RP : l; stride = a == 0 ? 1 : C::RP; }
+      else {
+        const int uu = l % NP, vv = l / NP;
+        if (a == 0)      { base = uu * C::RP + vv * C::PL; stride = 1; }
+        else if (a == 1) { base = uu + vv * C::PL;         stride = C::RP; }
+        else             { base = uu + vv * C::RP;         stride = C::PL; }
+      }
+      restrict_line<T>(X + p * C::TSZ + base, stride);
     }
     __syncthreads();
   }
   for (int e = threadIdx.x; e < C::PPC * C::CELL; e += blockDim.x) {
     const int p = e / C::CELL, l = e % C::CELL;
     if (!pis[p].valid) continue;
-    const PatchInfo& pi = pis[p];
-    const long long o = cell_offset_cells(gc, pi.c0[0] >> 1, pi.c0[1] >> 1, D == 3 ? pi.c0[2] >> 1 : 0) * C::CELL + l;
-    rc[o] = X[p * C::TSZ + node_of_cell<D>(0, l)];
+    const PInfo<D>& pi = pis[p];
+    const long long o =
+        cell_offset_cells(gc, pi.c0[0] >> 1, pi.c0[1] >> 1, D == 3 ? pi.c0[2] >> 1 : 0) * C::CELL + l;
+    rc[o] = X[p * C::TSZ + node_of_cell<D, T>(0, l)];
   }
 }
 
 // x_f += P e_c per parent cell
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D>::NT) prolong_kernel(const T* __restrict__ ec, T* __restrict__ xf,
-                                                             LevelGeom gf, LevelGeom gc) {
-  using C = Cfg<D>;
+__global__ void __launch_bounds__(Cfg<D, T>::NT) prolong_kernel(const T* __restrict__ ec, T* __restrict__ xf,
+                                                                LevelGeom gf, LevelGeom gc) {
+  using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
-  __shared__ PatchInfo pis[C::PPC];
-  const long long patch0 = (long long)blockIdx.x * C::PPC;
-  setup_patches<D, T>(pis, gf, 0, patch0, C::PPC);
+  __shared__ PInfo<D> pis[C::PPC];
+  setup_patches<D, T>(pis, gf, 0);
   for (int e = threadIdx.x; e < C::PPC * C::CELL; e += blockDim.x) {
     const int p = e / C::CELL, l = e % C::CELL;
-    const PatchInfo& pi = pis[p];
+    const PInfo<D>& pi = pis[p];
     T v = T(0);
     if (pi.valid)
       v = __ldg(ec + cell_offset_cells(gc, pi.c0[0] >> 1, pi.c0[1] >> 1, D == 3 ? pi.c0[2] >> 1 : 0) * C::CELL + l);
-    X[p * C::TSZ + node_of_cell<D>(0, l)] = v;
+    X[p * C::TSZ + node_of_cell<D, T>(0, l)] = v;
   }
   __syncthreads();
   // expand the last direction first so that the lines of earlier directions exist
@@ -661,27 +1400,28 @@ __global__ void __launch_bounds__(Cfg<D>::NT) prolong_kernel(const T* __restrict
     const int nl = (D == 2) ? (a == 1 ? NC : NP) : (a == 2 ? NC * NC : (a == 1 ? NC * NP : NP * NP));
     for (int e = threadIdx.x; e < C::PPC * nl; e += blockDim.x) {
       const int p = e / nl, li = e % nl;
-      int l;
-      if (D == 2) l = li;
-      else if (a == 0) l = li;
-      else l = (li % NC) + NP * (li / NC);
+      const int l = (D == 2 || a == 0) ? li : (li % NC) + NP * (li / NC);
       int base, stride;
-      line_geom<D>(a, l, base, stride);
-      T v[NC], w[NP];
-      load_line<NC>(X + p * C::TSZ + base, stride, v);
-      matvec<NP, NC, Prol<T>>(v, w);
-      store_line<NP>(X + p * C::TSZ + base, stride, w);
+      if (D == 2) { base = a == 0 ? l * C::RP : l; stride = a == 0 ? 1 : C::RP; }
+      else {
+        const int uu = l % NP, vv = l / NP;
+        if (a == 0)      { base = uu * C::RP + vv * C::PL; stride = 1; }
+        else if (a == 1) { base = uu + vv * C::PL;         stride = C::RP; }
+        else             { base = uu + vv * C::RP;         stride = C::PL; }
+      }
+      prolong_line<T>(X + p * C::TSZ + base, stride);
     }
     __syncthreads();
   }
-  store_patches<D, true>(xf, X, gf, pis, C::PPC, T(1));
+  store_patches<D, 1>(xf, X, pis, C::PPC, T(1));
 }
 
-// ---------------------------------------------------------------- host launchers
+// ---------------------------------------------------------------- host side
 template <int D, typename T>
 constexpr size_t smem_bytes(int ntensors, bool faces) {
-  using C = Cfg<D>;
-  return sizeof(T) * ((size_t)ntensors * C::PPC * C::TSZ + (faces ? 4 * (size_t)C::PPC * C::NFP : 0));
+  using C = Cfg<D, T>;
+  return sizeof(T) * ((size_t)ntensors * C::PPC * C::TSZ +
+                      (faces ? (size_t)C::PPC * C::FSZ + (C::STAGE ? (size_t)C::NBS : 0) : 0));
 }
 
 template <typename F>
@@ -689,24 +1429,40 @@ inline cudaError_t set_smem(F* f, size_t bytes) {
   return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// grid over the colour's patch lattice: (x-blocks of PPC patches, j1, j2)
+template <int D, typename T>
+inline dim3 patch_grid(const LevelGeom& g, int colour) {
+  using C = Cfg<D, T>;
+  const int m0 = g.n[0] / 2 - (colour & 1), m1 = g.n[1] / 2 - ((colour >> 1) & 1);
+  const int m2 = (D == 3) ? g.n[2] / 2 - ((colour >> 2) & 1) : 1;
+  return dim3((unsigned)((m0 + C::PPC - 1) / C::PPC), (unsigned)(m1 > 0 ? m1 : 0), (unsigned)(m2 > 0 ? m2 : 0));
+}
+
 template <int D, typename T>
 cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void* bm, cudaStream_t s) {
-  using C = Cfg<D>;
-  const long long np = num_patches(g, D, 0);
-  const unsigned grid = (unsigned)((np + C::PPC - 1) / C::PPC);
+  using C = Cfg<D, T>;
+  const dim3 grid = patch_grid<D, T>(g, 0);
   const size_t sm = smem_bytes<D, T>(2, true);
   cudaError_t e = set_smem(vmult_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
+  if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   vmult_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (T*)y, (const T*)bm, g);
   return cudaGetLastError();
 }
 
 template <int D, typename T>
 cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
-  using C = Cfg<D>;
-  const long long np = num_patches(g, D, colour);
-  const int patch_ctas = (int)((np + C::PPC - 1) / C::PPC);
-  int copy_ctas = 0;
+  using C = Cfg<D, T>;
+  const dim3 grid = patch_grid<D, T>(g, colour);
+  // no neighbour staging (and less shared memory, more CTAs) when x_in == 0
+  const size_t sm = xi ? smem_bytes<D, T>(1, true) : smem_bytes<D, T>(1, false) + sizeof(T) * C::PPC * C::FSZ;
+  cudaError_t e = set_smem(smooth_kernel<D, T>, smem_bytes<D, T>(1, true));
+  if (e != cudaSuccess) return e;
+  if (grid.x * grid.y * grid.z > 0) {
+    smooth_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   if (colour != 0) {
     long long cells = 0;
     for (int a = 0; a < D; ++a) {
@@ -715,26 +1471,21 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
       for (int bb = 0; bb < D; ++bb) if (bb != a) layer *= g.n[bb];
       cells += 2 * layer;
     }
-    long long elems = cells * C::CELL;
-    copy_ctas = (int)((elems + C::NT * 4 - 1) / (C::NT * 4));
-    if (copy_ctas < 1) copy_ctas = 1;
-    if (copy_ctas > 4 * 148) copy_ctas = 4 * 148;
+    const long long elems = cells * C::CELL;
+    long long blocks = (elems + 255) / 256;
+    if (blocks > 4 * 148) blocks = 4 * 148;
+    if (blocks < 1) blocks = 1;
+    copy_uncovered_kernel<D, T><<<(unsigned)blocks, 256, 0, s>>>((const T*)xi, (T*)xo, g, colour);
+    e = cudaGetLastError();
   }
-  const size_t sm = smem_bytes<D, T>(1, true);
-  cudaError_t e = set_smem(smooth_kernel<D, T>, sm);
-  if (e != cudaSuccess) return e;
-  if (patch_ctas + copy_ctas == 0) return cudaSuccess;
-  smooth_kernel<D, T><<<patch_ctas + copy_ctas, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour,
-                                                                  patch_ctas);
-  return cudaGetLastError();
+  return e;
 }
 
 template <int D, typename T>
 cudaError_t launch_additive(const void* r, void* x, const LevelGeom& g, int colour, double omega, cudaStream_t s) {
-  using C = Cfg<D>;
-  const long long np = num_patches(g, D, colour);
-  const int grid = (int)((np + C::PPC - 1) / C::PPC);
-  if (grid == 0) return cudaSuccess;
+  using C = Cfg<D, T>;
+  const dim3 grid = patch_grid<D, T>(g, colour);
+  if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   const size_t sm = smem_bytes<D, T>(1, false);
   cudaError_t e = set_smem(additive_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
@@ -745,9 +1496,9 @@ cudaError_t launch_additive(const void* r, void* x, const LevelGeom& g, int colo
 template <int D, typename T>
 cudaError_t launch_restrict(const void* x, const void* b, void* rc, const LevelGeom& gf, const LevelGeom& gc,
                             cudaStream_t s) {
-  using C = Cfg<D>;
-  const long long np = num_patches(gf, D, 0);
-  const unsigned grid = (unsigned)((np + C::PPC - 1) / C::PPC);
+  using C = Cfg<D, T>;
+  const dim3 grid = patch_grid<D, T>(gf, 0);
+  if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   const size_t sm = smem_bytes<D, T>(2, true);
   cudaError_t e = set_smem(restrict_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
@@ -757,9 +1508,9 @@ cudaError_t launch_restrict(const void* x, const void* b, void* rc, const LevelG
 
 template <int D, typename T>
 cudaError_t launch_prolong(const void* ec, void* xf, const LevelGeom& gf, const LevelGeom& gc, cudaStream_t s) {
-  using C = Cfg<D>;
-  const long long np = num_patches(gf, D, 0);
-  const unsigned grid = (unsigned)((np + C::PPC - 1) / C::PPC);
+  using C = Cfg<D, T>;
+  const dim3 grid = patch_grid<D, T>(gf, 0);
+  if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   const size_t sm = smem_bytes<D, T>(1, false);
   cudaError_t e = set_smem(prolong_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
@@ -768,15 +1519,73 @@ cudaError_t launch_prolong(const void* ec, void* xf, const LevelGeom& gf, const 
 }
 
 // runtime (dim, prec) dispatch
-#define IPMG_DISPATCH(dim, prec, FN, ...)                                  \
+#define IPMG_DISPATCH(dim, prec, FN, ...)                                               \
   ((dim) == 2 ? ((prec) == 0 ? FN<2, double>(__VA_ARGS__) : FN<2, float>(__VA_ARGS__)) \
               : ((prec) == 0 ? FN<3, double>(__VA_ARGS__) : FN<3, float>(__VA_ARGS__)))
 
-inline cudaError_t upload(const void* t64, const void* t32, size_t b64, size_t b32) {
-  if (b64 != sizeof(TabData<K, double>) || b32 != sizeof(TabData<K, float>)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemcpyToSymbol(c_tab64, t64, b64);
+// host copy of the tables in the exact device layout
+template <typename T>
+void fill_tab(TabData<K, T>& t, const FE1D& fe) {
+  std::memset(&t, 0, sizeof(t));
+  for (int i = 0; i < NC; ++i)
+    for (int j = 0; j < NC; ++j) t.M[i][j] = (T)fe.M[i * NC + j];
+  for (int v = 0; v < 4; ++v) {
+    for (int i = 0; i < NP; ++i)
+      for (int j = 0; j < NP; ++j) {
+        t.LP[v][i][j] = (T)fe.LP[v][i * NP + j];
+        t.S[v][i][j] = (T)fe.S[v][i * NP + j];
+        t.ST[v][j][i] = (T)fe.S[v][i * NP + j];
+      }
+    for (int i = 0; i < NP; ++i) t.lam[v][i] = (T)fe.lam[v][i];
+  }
+  for (int v = 0; v < 4; ++v)
+    for (int i = 0; i < NP; ++i)
+      for (int m = 0; m < NP; ++m) {
+        double acc = 0.0;   // (M^P S)[i][m] = sum_j M^P[i][j] S[j][m] = ((S^T M^P)^T)[i][m]
+        for (int j = 0; j < NP; ++j) acc += fe.MP[i * NP + j] * fe.S[v][j * NP + m];
+        t.MS[v][i][m] = (T)acc;
+      }
+  for (int i = 0; i < NP; ++i) {   // face coupling coefficients (C x_ext), see face_* kernels
+    t.CF[0][i] = (T)(i < NC ? -0.5 * fe.d0[i] - (i == 0 ? fe.gamma : 0.0) : 0.0);
+    t.CF[1][i] = (T)(i == 0 ? 0.5 : 0.0);
+    t.CF[2][i] = (T)(i >= NC ? 0.5 * fe.d1[i - NC] - (i == NP - 1 ? fe.gamma : 0.0) : 0.0);
+    t.CF[3][i] = (T)(i == NP - 1 ? -0.5 : 0.0);
+  }
+  for (int v = 0; v < 4; ++v)
+    for (int kd = 0; kd < 4; ++kd)
+      for (int m = 0; m < NP; ++m) {
+        double acc = 0.0;   // CH[v][kd][m] = sum_i S[v][i][m] CF[kd][i]
+        for (int i = 0; i < NP; ++i) {
+          const double cf = kd == 0 ? (i < NC ? -0.5 * fe.d0[i] - (i == 0 ? fe.gamma : 0.0) : 0.0)
+                          : kd == 1 ? (i == 0 ? 0.5 : 0.0)
+                          : kd == 2 ? (i >= NC ? 0.5 * fe.d1[i - NC] - (i == NP - 1 ? fe.gamma : 0.0) : 0.0)
+                                    : (i == NP - 1 ? -0.5 : 0.0);
+          acc += fe.S[v][i * NP + m] * cf;
+        }
+        t.CH[v][kd][m] = (T)acc;
+      }
+  for (int i = 0; i < NC; ++i) {
+    t.d0[i] = (T)fe.d0[i];
+    t.d1[i] = (T)fe.d1[i];
+    t.w[i] = (T)fe.w[i];
+  }
+  for (int i = 0; i < NP; ++i)
+    for (int j = 0; j < NC; ++j) {
+      t.P[i][j] = (T)fe.P[i * NC + j];
+      t.PT[j][i] = (T)fe.P[i * NC + j];
+    }
+  t.gamma = (T)fe.gamma;
+}
+
+inline cudaError_t upload(const FE1D& fe) {
+  if (fe.k != K) return cudaErrorInvalidValue;
+  static TabData<K, double> t64;
+  static TabData<K, float> t32;
+  fill_tab(t64, fe);
+  fill_tab(t32, fe);
+  cudaError_t e = cudaMemcpyToSymbol(c_tab64, &t64, sizeof(t64));
   if (e != cudaSuccess) return e;
-  return cudaMemcpyToSymbol(c_tab32, t32, b32);
+  return cudaMemcpyToSymbol(c_tab32, &t32, sizeof(t32));
 }
 inline cudaError_t vmult(int dim, int prec, const void* x, void* y, const LevelGeom& g, const void* bm, cudaStream_t s) {
   return IPMG_DISPATCH(dim, prec, launch_vmult, x, y, g, bm, s);
@@ -805,8 +1614,6 @@ extern "C++" ipmg::KernelSet IPMG_CAT(ipmg_kernel_set_k, IPMG_K)() {
   ipmg::KernelSet ks;
   ks.k = IPMG_K;
   ks.upload = ipmg::IPMG_KK::upload;
-  ks.tab_bytes64 = sizeof(ipmg::TabData<IPMG_K, double>);
-  ks.tab_bytes32 = sizeof(ipmg::TabData<IPMG_K, float>);
   ks.vmult = ipmg::IPMG_KK::vmult;
   ks.smooth = ipmg::IPMG_KK::smooth;
   ks.additive = ipmg::IPMG_KK::additive;

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libipmg.so")
+LIB_PATH = os.environ.get("IPMG_LIB", os.path.join(_HERE, "libipmg.so"))   # IPMG_LIB: A/B variants
 
 IPMG_OK = 0
 IPMG_ERR_NOT_CONVERGED = 7

@@ -64,7 +64,15 @@ def test_tables_match_oracle(k):
         assert np.abs(LP - blocks[v]).max() <= 1e-12 * np.abs(blocks[v]).max(), v
         S = ipmg.tables_1d(k, 7 + v).reshape(np_, np_)
         lam = ipmg.tables_1d(k, 11 + v)
-        assert np.all(np.diff(lam) >= 0) and lam[0] > 0
+        if v == 0:
+            # interior patch: reflection-symmetric problem; modes ordered [even | odd]
+            h = np_ // 2
+            assert np.all(np.diff(lam[:h]) >= 0) and np.all(np.diff(lam[h:]) >= 0)
+            assert np.abs(S[::-1, :h] - S[:, :h]).max() <= 1e-14 * np.abs(S).max()
+            assert np.abs(S[::-1, h:] + S[:, h:]).max() <= 1e-14 * np.abs(S).max()
+        else:
+            assert np.all(np.diff(lam) >= 0)
+        assert lam.min() > 0
         # generalized eigenpairs of the *oracle's* matrices: L S = M S Lambda, S^T M S = I
         assert np.abs(blocks[v] @ S - MP @ S * lam[None, :]).max() <= 1e-10 * lam.max()
         assert np.abs(S.T @ MP @ S - np.eye(np_)).max() <= 1e-11
