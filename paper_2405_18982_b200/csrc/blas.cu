@@ -37,20 +37,22 @@ __global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const TA* __re
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double* __restrict__ partial, int np,
+__global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double* __restrict__ partial, long long np,
                                                                 double* __restrict__ out) {
   __shared__ double sh[32];
   double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) s += partial[i];
+  for (long long i = threadIdx.x; i < np; i += blockDim.x) s += partial[i];
   s = block_sum<double>(s, sh);
   if (threadIdx.x == 0) *out = s;
 }
 
-// x += alpha p ; r -= alpha q ; partial ||r||^2   with alpha = s[i_rz] / s[i_pq]
+// x += alpha p ; r -= alpha q ; partial ||r||^2   with alpha = s[i_rz] / s[i_pq];
+// r32 != nullptr: also r32 = (float) r (the fp32 V-cycle input)
 __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                                              const double* __restrict__ p, const double* __restrict__ q,
                                                              long long n, const double* __restrict__ sc, int i_rz,
-                                                             int i_pq, double* __restrict__ partial) {
+                                                             int i_pq, double* __restrict__ partial,
+                                                             float* __restrict__ r32) {
   __shared__ double sh[32];
   const double alpha = sc[i_rz] / sc[i_pq];
   double s = 0.0;
@@ -58,10 +60,19 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
     x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
+    if (r32) r32[i] = (float)ri;
     s = fma(ri, ri, s);
   }
   s = block_sum<double>(s, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// p = (double) z32 + beta p (beta = s[i_new] / s[i_old]; i_old < 0: beta = 0)
+__global__ void cg_p32_kernel(double* __restrict__ p, const float* __restrict__ z, long long n,
+                              const double* __restrict__ sc, int i_new, int i_old) {
+  const double beta = i_old < 0 ? 0.0 : sc[i_new] / sc[i_old];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = i_old < 0 ? (double)z[i] : fma(beta, p[i], (double)z[i]);
 }
 
 // p = z + beta p, beta = s[i_new] / s[i_old]
@@ -201,14 +212,20 @@ cudaError_t dot_partial(int prec_a, int prec_b, const void* a, const void* b, lo
   return cudaGetLastError();
 }
 
-cudaError_t finalize(const double* partial, double* out, cudaStream_t s) {
-  finalize_kernel<<<1, RED_THREADS, 0, s>>>(partial, RED_BLOCKS, out);
+cudaError_t finalize(const double* partial, double* out, cudaStream_t s, long long np) {
+  finalize_kernel<<<1, RED_THREADS, 0, s>>>(partial, np < 0 ? RED_BLOCKS : np, out);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_update_p32(double* p, const float* z, long long n, const double* sc, int i_new, int i_old,
+                          cudaStream_t s) {
+  cg_p32_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, z, n, sc, i_new, i_old);
   return cudaGetLastError();
 }
 
 cudaError_t cg_update_xr(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
-                         int i_rz, int i_pq, double* partial, cudaStream_t s) {
-  cg_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial);
+                         int i_rz, int i_pq, double* partial, cudaStream_t s, float* r32) {
+  cg_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
   return cudaGetLastError();
 }
 

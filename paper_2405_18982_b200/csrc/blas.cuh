@@ -17,9 +17,11 @@ struct CoarseDesc {
 
 cudaError_t dot_partial(int prec_a, int prec_b, const void* a, const void* b, long long n, double* partial,
                         cudaStream_t s);
-cudaError_t finalize(const double* partial, double* out, cudaStream_t s);
+cudaError_t finalize(const double* partial, double* out, cudaStream_t s, long long np = -1);
 cudaError_t cg_update_xr(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
-                         int i_rz, int i_pq, double* partial, cudaStream_t s);
+                         int i_rz, int i_pq, double* partial, cudaStream_t s, float* r32 = nullptr);
+cudaError_t cg_update_p32(double* p, const float* z, long long n, const double* sc, int i_new, int i_old,
+                          cudaStream_t s);
 cudaError_t cg_update_p(double* p, const double* z, long long n, const double* sc, int i_new, int i_old,
                         cudaStream_t s);
 cudaError_t cast_f2d_dot(const float* zf, double* zd, const double* r, long long n, double* partial, cudaStream_t s);

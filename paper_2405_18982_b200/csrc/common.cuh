@@ -71,8 +71,10 @@ struct KernelSet {
   int k;
   cudaError_t (*upload)(const FE1D& fe);   // fill and upload the __constant__ tables
   // all launchers: prec 0 = double, 1 = float; dim 2 or 3
+  // y = A x (b_minus: y = b_minus - A x); dotp != nullptr: per-CTA partials of x.y,
+  // *nparts = their count (x == nullptr: size query only)
   cudaError_t (*vmult)(int dim, int prec, const void* x, void* y, const LevelGeom& g,
-                       const void* b_minus, cudaStream_t s);
+                       const void* b_minus, double* dotp, long long* nparts, cudaStream_t s);
   cudaError_t (*smooth)(int dim, int prec, const void* x_in, const void* b, void* x_out,
                         const LevelGeom& g, int colour, cudaStream_t s);
   cudaError_t (*additive)(int dim, int prec, const void* r, void* x, const LevelGeom& g, int colour,

@@ -63,6 +63,7 @@ struct ipmg_handle {
   // PCG workspace (finest level, fp64)
   double *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr;
   double *partial = nullptr, *scal = nullptr, *hpin = nullptr, *pattern = nullptr;
+  long long partial_len = 0;
   std::vector<void*> allocs;
   std::string err;
   // ---- instrumentation: launch counter and (optional) CUDA-event timing of
@@ -166,7 +167,7 @@ struct ipmg_handle {
     const void* r = b;
     if (!x_is_zero) {
       ipmg_status st = run(KC_VMULT, level, 3.0 * esize(prec) * ndofs[level], 1,
-                           [&] { return ks.vmult(dim, prec, x, rbuf, geom[level], b, stream); }, "residual");
+                           [&] { return ks.vmult(dim, prec, x, rbuf, geom[level], b, nullptr, nullptr, stream); }, "residual");
       if (st != IPMG_OK) return st;
       r = rbuf;
     } else {
@@ -375,7 +376,12 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   for (int p = 0; p < 2; ++p) h->scratch[p].assign(h->nlev, nullptr);
   // ---- f == 1 right-hand side pattern per level (w x w (x w) * h^d)
   h->pattern = (double*)h->dalloc(sizeof(double) * h->cell * h->nlev);
-  h->partial = (double*)h->dalloc(sizeof(double) * ipmg::RED_BLOCKS);
+  {
+    long long np = 0;   // fused p.q partials of the finest fp64 operator (one per CTA)
+    h->ks.vmult(h->dim, IPMG_FP64, nullptr, nullptr, h->geom[h->nlev - 1], nullptr, nullptr, &np, nullptr);
+    h->partial_len = np > ipmg::RED_BLOCKS ? np : ipmg::RED_BLOCKS;
+  }
+  h->partial = (double*)h->dalloc(sizeof(double) * h->partial_len);
   h->scal = (double*)h->dalloc(sizeof(double) * 8);
   if (!h->pattern || !h->partial || !h->scal) { h->err = "alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
   {
@@ -435,7 +441,8 @@ ipmg_status ipmg_vmult(ipmg_handle* h, int level, int precision, const void* x, 
       if (h->geom[0].n[a] % 2) return h->fail(IPMG_ERR_UNSUPPORTED, "ipmg_vmult: level 0 with odd cell count");
   }
   return h->run(KC_VMULT, level, 2.0 * h->esize(precision) * h->ndofs[level], 1,
-                [&] { return h->ks.vmult(h->dim, precision, x, y, h->geom[level], nullptr, h->stream); }, "vmult");
+                [&] { return h->ks.vmult(h->dim, precision, x, y, h->geom[level], nullptr, nullptr, nullptr, h->stream); },
+                "vmult");
 }
 
 ipmg_status ipmg_smooth_colour(ipmg_handle* h, int level, int precision, const void* x_in, const void* b,
@@ -559,20 +566,42 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
   int it = 0;
   bool conv = (r0 == 0.0);
   if (!conv) {
-    int cur = 0;
-    st = h->vcycle(h->r, h->z, h->partial);
-    if (st != IPMG_OK) return st;
-    h->n_launches += 1;
-    CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
-    CK(cudaMemcpyAsync(h->p, h->z, n * 8, cudaMemcpyDeviceToDevice, s), "copy p");
-    while (it < max_it) {
-      st = h->run(KC_VMULT, L, 16.0 * n, 1,
-                  [&] { return h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, s); }, "vmult");
+    // mixed precision: the fp32 V-cycle input r32 is written by
+    // the fused x/r update, z stays fp32 (p = (double) z + beta p), and p.q is
+    // fused into the operator kernel.
+    const bool mixed = h->cfg.vcycle_precision == IPMG_FP32;
+    if (mixed) {
+      st = h->ensure_vcycle(IPMG_FP32);
       if (st != IPMG_OK) return st;
-      h->n_launches += 4;
-      CK(ipmg::dot_partial(0, 0, h->p, h->q, n, h->partial, s), "dot");
-      CK(ipmg::finalize(h->partial, h->scal + 2, s), "finalize");
-      CK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s), "update");
+    }
+    float* r32 = mixed ? (float*)h->vb[IPMG_FP32][L] : nullptr;
+    const float* z32 = mixed ? (const float*)h->vx1[IPMG_FP32][L] : nullptr;
+    int cur = 0;
+    if (mixed) {
+      h->n_launches += 1;
+      CK(ipmg::cast(0, 1, h->r, r32, n, s), "cast");
+      st = h->vcycle_level(L, IPMG_FP32);
+      if (st != IPMG_OK) return st;
+      h->n_launches += 3;
+      CK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), "dot");
+      CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
+      CK(ipmg::cg_update_p32(h->p, z32, n, h->scal, cur, -1, s), "p = z");
+    } else {
+      st = h->vcycle(h->r, h->z, h->partial);
+      if (st != IPMG_OK) return st;
+      h->n_launches += 1;
+      CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
+      CK(cudaMemcpyAsync(h->p, h->z, n * 8, cudaMemcpyDeviceToDevice, s), "copy p");
+    }
+    while (it < max_it) {
+      long long nparts = 0;
+      st = h->run(KC_VMULT, L, 16.0 * n, 1,
+                  [&] { return h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, h->partial, &nparts, s); },
+                  "vmult");
+      if (st != IPMG_OK) return st;
+      h->n_launches += 3;
+      CK(ipmg::finalize(h->partial, h->scal + 2, s, nparts), "finalize");
+      CK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s, r32), "update");
       CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
       CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
       CK(cudaStreamSynchronize(s), "sync");
@@ -580,11 +609,20 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       const double rn = std::sqrt(h->hpin[0]);
       hist.push_back(rn);
       if (rn <= rtol * r0) { conv = true; break; }
-      st = h->vcycle(h->r, h->z, h->partial);
-      if (st != IPMG_OK) return st;
-      h->n_launches += 2;
-      CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
-      CK(ipmg::cg_update_p(h->p, h->z, n, h->scal, 1 - cur, cur, s), "update p");
+      if (mixed) {
+        st = h->vcycle_level(L, IPMG_FP32);
+        if (st != IPMG_OK) return st;
+        h->n_launches += 3;
+        CK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), "dot");
+        CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
+        CK(ipmg::cg_update_p32(h->p, z32, n, h->scal, 1 - cur, cur, s), "update p");
+      } else {
+        st = h->vcycle(h->r, h->z, h->partial);
+        if (st != IPMG_OK) return st;
+        h->n_launches += 2;
+        CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
+        CK(ipmg::cg_update_p(h->p, h->z, n, h->scal, 1 - cur, cur, s), "update p");
+      }
       cur = 1 - cur;
     }
   }

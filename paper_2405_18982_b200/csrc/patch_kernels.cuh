@@ -994,10 +994,12 @@ __device__ __forceinline__ void store_rows(T* __restrict__ dst, const T* __restr
 // element j of a line -> cell q(l, j), in-cell offset; per store instruction the
 // warp's consecutive lines are consecutive addresses (coalesced)
 template <int D, int MODE, int R, typename T>
-__device__ __forceinline__ void store_last_lines(T* __restrict__ dst, const T* __restrict__ bm, const PInfo<D>& pi,
-                                                 int g, T scale, const T (&v)[R][NP]) {
+__device__ __forceinline__ double store_last_lines(T* __restrict__ dst, const T* __restrict__ bm, const PInfo<D>& pi,
+                                                   int g, T scale, const T (&v)[R][NP],
+                                                   const T* __restrict__ xdot = nullptr) {
   using C = Cfg<D, T>;
-  if (!pi.valid) return;
+  double dot = 0.0;   // sum xdot[o] * stored value (the fused p.q of CG), when xdot != nullptr
+  if (!pi.valid) return dot;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int l = g + r * C::G;
@@ -1013,8 +1015,10 @@ __device__ __forceinline__ void store_last_lines(T* __restrict__ dst, const T* _
       if (MODE == 1) val += dst[o];
       else if (MODE == 2) val = __ldg(bm + o) - val;
       dst[o] = val;
+      if (xdot != nullptr) dot = fma((double)__ldg(xdot + o), (double)val, dot);
     }
   }
+  return dot;
 }
 
 // ---------------------------------------------------------------- volume term
@@ -1185,7 +1189,8 @@ __device__ __forceinline__ void my_rows(const T* __restrict__ src, const PInfo<D
 // y = hs * A x   or, with bminus != nullptr, y = bminus - hs * A x
 template <int D, typename T>
 __global__ void __launch_bounds__(Cfg<D, T>::NT) vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                              const T* __restrict__ bminus, LevelGeom g) {
+                                                              const T* __restrict__ bminus, LevelGeom g,
+                                                              double* __restrict__ dot_partial) {
   using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
@@ -1205,14 +1210,28 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) vmult_kernel(const T* __restric
 #endif
   vol_pre<D, true>(xr, X, T1, F, pis, C::PPC);
   const T hs = T(g.hs);
+  double dot = 0.0;
+  const T* xd = dot_partial ? x : nullptr;
   if (bminus == nullptr)
     vol_last<D, true>(X, T1, F, pis, C::PPC, [&](int p, int gg, int, int, int, const T (&yy)[C::R][NP]) {
-      store_last_lines<D, 0, C::R>(y, (const T*)nullptr, pis[p], gg, hs, yy);
+      dot += store_last_lines<D, 0, C::R>(y, (const T*)nullptr, pis[p], gg, hs, yy, xd);
     });
   else
     vol_last<D, true>(X, T1, F, pis, C::PPC, [&](int p, int gg, int, int, int, const T (&yy)[C::R][NP]) {
-      store_last_lines<D, 2, C::R>(y, bminus, pis[p], gg, hs, yy);
+      dot += store_last_lines<D, 2, C::R>(y, bminus, pis[p], gg, hs, yy, xd);
     });
+  if (dot_partial != nullptr) {
+    // fused x.y (the p.q of CG): deterministic block partial, fixed tree
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    __shared__ double wsum[C::NT / 32];
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < C::NT / 32; ++w) t += wsum[w];
+      dot_partial[blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z)] = t;
+    }
+  }
 }
 
 // one colour of the multiplicative full-kernel smoother (replacement form):
@@ -1339,28 +1358,37 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) restrict_kernel(const T* __rest
       store_lines<NP, C::R>(X + base, gap, stride, yy);
     });
     __syncthreads();
-    // T1 <- b ; X <- T1 - hs X
-    load_patches<D>(T1, b, pis, C::PPC, T(1));
-    __syncthreads();
-    for (int e = threadIdx.x; e < C::PPC * C::TSZ; e += blockDim.x) X[e] = T1[e] - hs * X[e];
-  } else {
-    load_patches<D>(X, b, pis, C::PPC, T(1));
   }
+  // residual rows r = b - hs (A x) (b rows straight from global) and P^T along x
+  // (NC outputs into the first NC entries of each row)
+  for_groups<D, T>(0, C::PPC, [&](int p, int g, int base, int gap, int stride) {
+    T br[C::R][NP], w[C::R][NC];
+    load_rows<D, C::R>(b, pis[p], g, T(1), br);
+    if (x != nullptr) {
+      T v[C::R][NP];
+      load_lines<NP, C::R>(X + base, gap, stride, v);
+#pragma unroll
+      for (int r = 0; r < C::R; ++r)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) br[r][j] = fma_(-hs, v[r][j], br[r][j]);
+    }
+    mv<NC, NP, ProlT<T>, C::R>(br, w);
+    store_lines<NC, C::R>(X + base, gap, stride, w);
+  });
   __syncthreads();
-  // P^T along x (all lines), then y (lines with i0 < NC), then z (i0, i1 < NC)
+  // P^T along y (lines with i0 < NC), then z (lines with i0, i1 < NC)
 #pragma unroll 1
-  for (int a = 0; a < D; ++a) {
-    const int nl = (D == 2) ? (a == 0 ? NP : NC) : (a == 0 ? NP * NP : (a == 1 ? NC * NP : NC * NC));
+  for (int a = 1; a < D; ++a) {
+    const int nl = (D == 2) ? NC : (a == 1 ? NC * NP : NC * NC);
     for (int e = threadIdx.x; e < C::PPC * nl; e += blockDim.x) {
       const int p = e / nl, li = e % nl;
-      const int l = (D == 2 || a == 0) ? li : (li % NC) + NP * (li / NC);
+      const int l = (D == 2) ? li : (li % NC) + NP * (li / NC);
       int base, stride;
-      if (D == 2) { base = a == 0 ? l * C::RP : l; stride = a == 0 ? 1 : C::RP; }
+      if (D == 2) { base = l; stride = C::RP; }
       else {
         const int uu = l % NP, vv = l / NP;
-        if (a == 0)      { base = uu * C::RP + vv * C::PL; stride = 1; }
-        else if (a == 1) { base = uu + vv * C::PL;         stride = C::RP; }
-        else             { base = uu + vv * C::RP;         stride = C::PL; }
+        if (a == 1) { base = uu + vv * C::PL; stride = C::RP; }
+        else        { base = uu + vv * C::RP; stride = C::PL; }
       }
       restrict_line<T>(X + p * C::TSZ + base, stride);
     }
@@ -1396,24 +1424,29 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) prolong_kernel(const T* __restr
   __syncthreads();
   // expand the last direction first so that the lines of earlier directions exist
 #pragma unroll 1
-  for (int a = D - 1; a >= 0; --a) {
-    const int nl = (D == 2) ? (a == 1 ? NC : NP) : (a == 2 ? NC * NC : (a == 1 ? NC * NP : NP * NP));
+  for (int a = D - 1; a >= 1; --a) {
+    const int nl = (D == 2) ? NC : (a == 2 ? NC * NC : NC * NP);
     for (int e = threadIdx.x; e < C::PPC * nl; e += blockDim.x) {
       const int p = e / nl, li = e % nl;
-      const int l = (D == 2 || a == 0) ? li : (li % NC) + NP * (li / NC);
+      const int l = (D == 2) ? li : (li % NC) + NP * (li / NC);
       int base, stride;
-      if (D == 2) { base = a == 0 ? l * C::RP : l; stride = a == 0 ? 1 : C::RP; }
+      if (D == 2) { base = l; stride = C::RP; }
       else {
         const int uu = l % NP, vv = l / NP;
-        if (a == 0)      { base = uu * C::RP + vv * C::PL; stride = 1; }
-        else if (a == 1) { base = uu + vv * C::PL;         stride = C::RP; }
-        else             { base = uu + vv * C::RP;         stride = C::PL; }
+        if (a == 1) { base = uu + vv * C::PL; stride = C::RP; }
+        else        { base = uu + vv * C::RP; stride = C::PL; }
       }
       prolong_line<T>(X + p * C::TSZ + base, stride);
     }
     __syncthreads();
   }
-  store_patches<D, 1>(xf, X, pis, C::PPC, T(1));
+  // x expansion, added straight into the fine rows
+  for_groups<D, T>(0, C::PPC, [&](int p, int g, int base, int gap, int stride) {
+    T v[C::R][NC], w[C::R][NP];
+    load_lines<NC, C::R>(X + base, gap, stride, v);
+    mv<NP, NC, Prol<T>, C::R>(v, w);
+    store_rows<D, 1, C::R>(xf, (const T*)nullptr, pis[p], g, T(1), w);
+  });
 }
 
 // ---------------------------------------------------------------- host side
@@ -1439,14 +1472,17 @@ inline dim3 patch_grid(const LevelGeom& g, int colour) {
 }
 
 template <int D, typename T>
-cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void* bm, cudaStream_t s) {
+cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp, long long* nparts,
+                         cudaStream_t s) {
   using C = Cfg<D, T>;
   const dim3 grid = patch_grid<D, T>(g, 0);
+  if (nparts) *nparts = (long long)grid.x * grid.y * grid.z;
+  if (x == nullptr) return cudaSuccess;   // size query
   const size_t sm = smem_bytes<D, T>(2, true);
   cudaError_t e = set_smem(vmult_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
   if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
-  vmult_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (T*)y, (const T*)bm, g);
+  vmult_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (T*)y, (const T*)bm, g, dotp);
   return cudaGetLastError();
 }
 
@@ -1587,8 +1623,9 @@ inline cudaError_t upload(const FE1D& fe) {
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(c_tab32, &t32, sizeof(t32));
 }
-inline cudaError_t vmult(int dim, int prec, const void* x, void* y, const LevelGeom& g, const void* bm, cudaStream_t s) {
-  return IPMG_DISPATCH(dim, prec, launch_vmult, x, y, g, bm, s);
+inline cudaError_t vmult(int dim, int prec, const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp,
+                         long long* nparts, cudaStream_t s) {
+  return IPMG_DISPATCH(dim, prec, launch_vmult, x, y, g, bm, dotp, nparts, s);
 }
 inline cudaError_t smooth(int dim, int prec, const void* xi, const void* b, void* xo, const LevelGeom& g, int c,
                           cudaStream_t s) {
