@@ -59,6 +59,16 @@ typedef enum { IPMG_KERNEL_FULL = 0 } ipmg_kernel;
  * configs[4] (damped, omega default 1/2^d, reading A17). */
 typedef enum { IPMG_MULTIPLICATIVE = 0, IPMG_ADDITIVE = 1 } ipmg_smoother;
 
+/* Communicator of the slab decomposition (DESIGN.md
+ * "Multi-GPU"): rank r of R owns a contiguous range of cell layers along the
+ * slowest axis (y in 2D, z in 3D) on every level whose global layer count is
+ * a multiple of 2R ("distributed" levels); coarser levels are replicated and
+ * computed redundantly on every rank.  Library-owned; created by
+ * ipmg_comm_create_nccl (one process per GPU) or ipmg_comm_create_local (an
+ * in-process team: one handle per host thread, used to test the distributed
+ * path on a single device). */
+typedef struct ipmg_comm ipmg_comm;
+
 typedef struct {
   int dim;                  /* 2 or 3 (else IPMG_ERR_INVALID_ARG)                         */
   int degree;               /* k = 1..7 (else IPMG_ERR_UNSUPPORTED)                       */
@@ -73,6 +83,7 @@ typedef struct {
   double penalty_scale;     /* gamma = penalty_scale * k(k+1)(1/h+ + 1/h-); default 1     */
   int device;               /* CUDA device ordinal                                         */
   void *cuda_stream;        /* cudaStream_t all work is enqueued on                        */
+  ipmg_comm *comm;          /* NULL: one GPU; else this rank's communicator (not owned)    */
 } ipmg_config;
 
 typedef struct ipmg_handle ipmg_handle;
@@ -98,9 +109,41 @@ void ipmg_config_default(ipmg_config *cfg);
 ipmg_status ipmg_create(const ipmg_config *cfg, ipmg_handle **out);
 ipmg_status ipmg_destroy(ipmg_handle *h);
 
-/* Level geometry.  ndofs = cells * (k+1)^d; cells[3] (cells[2] = 1 in 2D); hsize = h0/2^l. */
+/* Level geometry of THIS rank.  ndofs = local cells * (k+1)^d; cells[3] local cells
+ * (cells[2] = 1 in 2D); hsize = h0/2^l.  On a distributed level the local vector
+ * is the contiguous range [zoff * layer, (zoff + cells[S]) * layer) of the global
+ * library-order vector (layer = dofs per cell layer of the slowest axis S). */
 ipmg_status ipmg_level_info(const ipmg_handle *h, int level, int64_t *ndofs, int cells[3],
                             double *hsize);
+
+/* Partition of a level on this rank: *distributed (1: local slab, 0: replicated),
+ * *zoff (first global cell layer of the slab along the slowest axis), *nglob
+ * (global cell layers along it). */
+ipmg_status ipmg_level_partition(const ipmg_handle *h, int level, int *distributed, int *zoff,
+                                 int *nglob);
+
+/* HOST-ONLY: the partition rule itself (no GPU needed).  out[0] distributed,
+ * out[1] zoff, out[2] local layers, out[3] global layers of `level` for `rank`
+ * of `nranks`.  Rule: level l >= 1 is distributed iff its global layer count
+ * along the slowest axis is a multiple of 2*nranks (every rank owns an even
+ * number >= 2 of layers, so colour-0 patches and parent cells never straddle
+ * ranks); with nranks = 1 every level is "distributed" (zoff 0). */
+ipmg_status ipmg_partition(int dim, const int coarse_cells[3], int n_levels, int nranks, int rank,
+                           int level, int out[4]);
+
+/* Communicators.  ipmg_nccl_unique_id writes 128 bytes (host) that rank 0
+ * broadcasts (e.g. through torch.distributed) to every rank, which then calls
+ * ipmg_comm_create_nccl with its rank, the world size and its CUDA device
+ * (libnccl.so.2 is resolved at run time; IPMG_ERR_NCCL if absent or on NCCL
+ * errors).  ipmg_comm_create_local fills out[0..nranks-1] with the members of
+ * an in-process team on devices[r] (NULL: all device 0); member r must be
+ * driven by its own host thread.  A peer that fails or stalls for 120 s makes
+ * the others return IPMG_ERR_NCCL instead of hanging. */
+ipmg_status ipmg_nccl_unique_id(void *id128);
+ipmg_status ipmg_comm_create_nccl(const void *id128, int rank, int nranks, int device,
+                                  ipmg_comm **out);
+ipmg_status ipmg_comm_create_local(int nranks, const int *devices, ipmg_comm **out);
+ipmg_status ipmg_comm_destroy(ipmg_comm *c);
 
 /* y = A_l x, the SIPG operator on level l applied matrix-free, patch-wise over
  * the colour-0 vertex patches (Fig. 1).  x, y: level l. */

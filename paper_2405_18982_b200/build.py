@@ -24,8 +24,8 @@ CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xpt
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-I" + INCLUDE, "-I" + CSRC, "-I/usr/local/cuda/include"]
 
 SOURCES_CU = ["kernels_k%d.cu" % k for k in range(1, 8)] + ["blas.cu"]
-SOURCES_CXX = ["fe1d.cpp", "ipmg.cpp"]
-HEADERS = ["common.cuh", "patch_kernels.cuh", "blas.cuh", "fe1d.hpp"]
+SOURCES_CXX = ["fe1d.cpp", "comm.cpp", "ipmg.cpp"]
+HEADERS = ["common.cuh", "patch_kernels.cuh", "blas.cuh", "fe1d.hpp", "comm.hpp"]
 
 
 def _stale(obj, deps):
@@ -71,7 +71,7 @@ def build(force=False, verbose=False, jobs=None, defines=(), tag=""):
             sys.stdout.write(o)
     objs = [os.path.join(obj_dir, s + ".o") for s in SOURCES_CU + SOURCES_CXX]
     if force or tasks or _stale(lib, objs):
-        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs, os.path.join(obj_dir, "link.log"))
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs + ["-ldl", "-lpthread"], os.path.join(obj_dir, "link.log"))
     return lib
 
 

@@ -190,6 +190,32 @@ __global__ void coarse_fd_kernel(const T* __restrict__ b, T* __restrict__ x, Coa
   }
 }
 
+// buf = sum over ranks in rank order; the own block is buf itself, the others
+// are packed (rank order, own skipped) in scratch -- deterministic and
+// identical on every rank
+template <typename T>
+__global__ void sum_ranks_kernel(T* __restrict__ buf, const T* __restrict__ scratch, int nranks, int rank,
+                                 long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    T s = T(0);
+    int j = 0;
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) s += buf[i];
+      else s += scratch[(long long)(j++) * n + i];
+    }
+    buf[i] = s;
+  }
+}
+
+// out[v] = sum_r g[r * nv + v] in rank order (allgathered per-rank scalars)
+__global__ void gather_sum_kernel(const double* __restrict__ g, int nranks, int nv, double* __restrict__ out) {
+  const int v = threadIdx.x;
+  if (v >= nv) return;
+  double s = 0.0;
+  for (int r = 0; r < nranks; ++r) s += g[r * nv + v];
+  out[v] = s;
+}
+
 inline int grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   if (g > 8 * 148) g = 8 * 148;
@@ -259,6 +285,19 @@ cudaError_t permute(int prec, bool to_cellwise, const void* in, void* out, const
     if (to_cellwise) permute_kernel<float, true><<<grid, 256, 0, s>>>((const float*)in, (float*)out, g, cell, n);
     else permute_kernel<float, false><<<grid, 256, 0, s>>>((const float*)in, (float*)out, g, cell, n);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t sum_ranks(int prec, void* buf, const void* scratch, int nranks, int rank, long long n, cudaStream_t s) {
+  if (prec == 0)
+    sum_ranks_kernel<double><<<grid_for(n, 256), 256, 0, s>>>((double*)buf, (const double*)scratch, nranks, rank, n);
+  else
+    sum_ranks_kernel<float><<<grid_for(n, 256), 256, 0, s>>>((float*)buf, (const float*)scratch, nranks, rank, n);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_sum(const double* g, int nranks, int nv, double* out, cudaStream_t s) {
+  gather_sum_kernel<<<1, 32, 0, s>>>(g, nranks, nv, out);
   return cudaGetLastError();
 }
 

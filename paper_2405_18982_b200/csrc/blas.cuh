@@ -28,6 +28,8 @@ cudaError_t cast_f2d_dot(const float* zf, double* zd, const double* r, long long
 cudaError_t cast(int prec_in, int prec_out, const void* in, void* out, long long n, cudaStream_t s);
 cudaError_t permute(int prec, bool to_cellwise, const void* in, void* out, const LevelGeom& g, int cell, long long n,
                     cudaStream_t s);
+cudaError_t sum_ranks(int prec, void* buf, const void* scratch, int nranks, int rank, long long n, cudaStream_t s);
+cudaError_t gather_sum(const double* g, int nranks, int nv, double* out, cudaStream_t s);
 cudaError_t pattern_fill(double* b, const double* pat, int cell, long long n, cudaStream_t s);
 cudaError_t coarse_solve(int prec, const void* b, void* x, const CoarseDesc& cd, const void* const S[3],
                          const void* const L[3], cudaStream_t s);

@@ -16,13 +16,26 @@
 
 namespace ipmg {
 
+// Slab decomposition: a rank owns the cells
+// zoff..zoff+n[S]-1 of the slowest axis S = d-1 (y in 2D, z in 3D) out of
+// nglob; zoff and n[S] are even, so the local cells are one contiguous range of
+// the parent-grouped vector.  Internal vectors of a distributed level carry one
+// ghost parent layer (2 cell layers) below and above the local range, addressed
+// by the same cell_offset_cells with local coordinates -2..-1 and n[S]..n[S]+1
+// (floor shifts give negative / past-the-end offsets).  A single GPU is the
+// special case zoff = 0, nglob = n[S].
 struct LevelGeom {
-  int n[3];            // cells per direction
+  int n[3];            // LOCAL cells per direction (n[2] = 1 in 2D)
   int grouped;         // 1: parent-grouped layout, 0: lexicographic cells
-  long long ncells;
+  long long ncells;    // local cells
   double hs;           // h^(d-2)
   double hinv;         // h^(2-d)
+  int zoff;            // global index of local cell 0 along the slowest axis
+  int nglob;           // global cells along the slowest axis
 };
+
+// "no neighbour" marker of patch neighbour offsets (ghost offsets are negative)
+constexpr long long NO_NB = (long long)(-0x7fffffffffffffffLL - 1);
 
 __host__ __device__ __forceinline__ long long cell_offset_cells(const LevelGeom& g, int cx, int cy,
                                                                 int cz) {

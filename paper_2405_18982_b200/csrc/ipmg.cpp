@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "blas.cuh"
+#include "comm.hpp"
 #include "common.cuh"
 #include "fe1d.hpp"
 
@@ -27,6 +28,17 @@ ipmg::KernelSet ipmg_kernel_set_k7();
 namespace {
 
 std::string g_create_error;
+
+// partition rule of the slab decomposition (ipmg.h ipmg_partition)
+void partition_rule(int dim, const int cc[3], int l, int nranks, int rank, int out[4]) {
+  const int S = dim - 1;
+  const long long ng = (long long)cc[S] << l;
+  const int dist = nranks == 1 ? 1 : (l >= 1 && ng % (2LL * nranks) == 0 ? 1 : 0);
+  out[0] = dist;
+  out[3] = (int)ng;
+  out[2] = dist ? (int)(ng / nranks) : (int)ng;
+  out[1] = dist ? rank * out[2] : 0;
+}
 
 ipmg::KernelSet kernel_set(int k) {
   switch (k) {
@@ -66,6 +78,13 @@ struct ipmg_handle {
   long long partial_len = 0;
   std::vector<void*> allocs;
   std::string err;
+  // ---- slab decomposition
+  ipmg_comm* comm = nullptr;
+  int rank = 0, nranks = 1;
+  std::vector<int> dist;              // level distributed over the ranks (1) or replicated (0)
+  std::vector<long long> ghost;       // elements of one ghost parent layer (0: no ghosts)
+  double* gbuf = nullptr;             // allgathered per-rank scalars
+  std::vector<void*> gsc[2][3];       // ghosted copies of caller vectors (API calls), [prec][slot][level]
   // ---- instrumentation: launch counter and (optional) CUDA-event timing of
   // the finest-level kernels, per kernel class (ipmg_profile*)
   long long n_launches = 0;
@@ -121,10 +140,49 @@ struct ipmg_handle {
     return ptr;
   }
   size_t esize(int prec) const { return prec == IPMG_FP64 ? 8 : 4; }
+  // level vector with a ghost parent layer before and after the local range
+  // (distributed levels with several ranks; plain otherwise)
+  void* valloc(int level, int prec) {
+    const long long gh = ghost[level];
+    char* base = (char*)dalloc((size_t)(ndofs[level] + 2 * gh) * esize(prec));
+    return base ? base + gh * esize(prec) : nullptr;
+  }
   ipmg_status ensure_scratch(int prec, int level) {
     if (scratch[prec][level]) return IPMG_OK;
-    scratch[prec][level] = dalloc(ndofs[level] * esize(prec));
+    scratch[prec][level] = valloc(level, prec);
     return scratch[prec][level] ? IPMG_OK : fail(IPMG_ERR_OUT_OF_MEMORY, "scratch allocation failed");
+  }
+  // ------------------------------------------------------------ communication
+  // ghost parent layers of x from the neighbour ranks (x: a valloc'ed vector)
+  ipmg_status halo(int level, int prec, const void* x) {
+    if (!comm || ghost[level] == 0) return IPMG_OK;
+    const size_t es = esize(prec), gb = (size_t)ghost[level] * es, nb = (size_t)ndofs[level] * es;
+    char* xb = (char*)const_cast<void*>(x);
+    if (!comm->halo(xb, xb + nb - gb, xb - gb, xb + nb, gb, stream)) return fail(IPMG_ERR_NCCL, comm->err);
+    return IPMG_OK;
+  }
+  // device scalar -> its sum over the ranks (rank order, identical everywhere)
+  ipmg_status allsum(double* slot) {
+    if (!comm || nranks == 1) return IPMG_OK;
+    if (!comm->allgather(slot, gbuf, sizeof(double), stream)) return fail(IPMG_ERR_NCCL, comm->err);
+    n_launches += 1;
+    return cuda(ipmg::gather_sum(gbuf, nranks, 1, slot, stream), "gather_sum");
+  }
+  // restriction into a replicated level from a distributed one: every rank
+  // writes its parents into a zeroed vector, the sum over ranks assembles it
+  bool transition(int l) const { return nranks > 1 && l >= 1 && dist[l] && !dist[l - 1]; }
+  // caller vector -> ghosted copy with current ghosts (distributed levels)
+  ipmg_status ghosted(int level, int prec, int slot, const void* v, const void** out) {
+    *out = v;
+    if (!v || ghost[level] == 0) return IPMG_OK;
+    std::vector<void*>& g = gsc[prec][slot];
+    if (g.empty()) g.assign(nlev, nullptr);
+    if (!g[level] && !(g[level] = valloc(level, prec))) return fail(IPMG_ERR_OUT_OF_MEMORY, "ghosted copy allocation failed");
+    ipmg_status st = cuda(cudaMemcpyAsync(g[level], v, ndofs[level] * esize(prec), cudaMemcpyDeviceToDevice, stream), "copy");
+    if (st != IPMG_OK) return st;
+    st = halo(level, prec, g[level]);
+    *out = g[level];
+    return st;
   }
   ipmg_status ensure_vcycle(int prec) {
     if (!vx0[prec].empty() && vx0[prec][0]) return IPMG_OK;
@@ -132,9 +190,9 @@ struct ipmg_handle {
     vx1[prec].assign(nlev, nullptr);
     vb[prec].assign(nlev, nullptr);
     for (int l = 0; l < nlev; ++l) {
-      vx0[prec][l] = dalloc(ndofs[l] * esize(prec));
-      vx1[prec][l] = dalloc(ndofs[l] * esize(prec));
-      vb[prec][l] = dalloc(ndofs[l] * esize(prec));
+      vx0[prec][l] = valloc(l, prec);
+      vx1[prec][l] = valloc(l, prec);
+      vb[prec][l] = valloc(l, prec);
       if (!vx0[prec][l] || !vx1[prec][l] || !vb[prec][l])
         return fail(IPMG_ERR_OUT_OF_MEMORY, "V-cycle workspace allocation failed");
     }
@@ -153,7 +211,12 @@ struct ipmg_handle {
     void* nxt = other;
     for (int i = 0; i < ncol; ++i) {
       const int c = reverse ? ncol - 1 - i : i;
-      ipmg_status st = smooth_colour(level, prec, (i == 0 && x_is_zero) ? nullptr : cur, b, nxt, c);
+      const bool zero = i == 0 && x_is_zero;
+      if (!zero) {   // every colour reads face traces of the neighbour slabs
+        ipmg_status st = halo(level, prec, cur);
+        if (st != IPMG_OK) return st;
+      }
+      ipmg_status st = smooth_colour(level, prec, zero ? nullptr : cur, b, nxt, c);
       if (st != IPMG_OK) return st;
       std::swap(cur, nxt);
     }
@@ -166,8 +229,12 @@ struct ipmg_handle {
   ipmg_status smooth_add(int level, int prec, void* x, void* rbuf, const void* b, bool x_is_zero) {
     const void* r = b;
     if (!x_is_zero) {
-      ipmg_status st = run(KC_VMULT, level, 3.0 * esize(prec) * ndofs[level], 1,
-                           [&] { return ks.vmult(dim, prec, x, rbuf, geom[level], b, nullptr, nullptr, stream); }, "residual");
+      ipmg_status st = halo(level, prec, x);
+      if (st != IPMG_OK) return st;
+      st = run(KC_VMULT, level, 3.0 * esize(prec) * ndofs[level], 1,
+               [&] { return ks.vmult(dim, prec, x, rbuf, geom[level], b, nullptr, nullptr, stream); }, "residual");
+      if (st != IPMG_OK) return st;
+      st = halo(level, prec, rbuf);   // straddling patches read r on the ghost cells
       if (st != IPMG_OK) return st;
       r = rbuf;
     } else {
@@ -189,20 +256,35 @@ struct ipmg_handle {
   }
   // one V-cycle on level l of the workspace of precision prec: input vb[l],
   // output vx1[l]
+  // r_c = P^T (b - A x) (x ghosts current), with the distributed -> replicated transition
+  ipmg_status restrict_to(int l, int prec, const void* x, const void* b, void* rc) {
+    ipmg_status st;
+    if (transition(l)) {
+      st = cuda(cudaMemsetAsync(rc, 0, ndofs[l - 1] * esize(prec), stream), "memset");
+      if (st != IPMG_OK) return st;
+    }
+    st = run(KC_RESTRICT, l, esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]), 1,
+             [&] { return ks.restrict_(dim, prec, x, b, rc, geom[l], geom[l - 1], stream); }, "restrict");
+    if (st != IPMG_OK || !transition(l)) return st;
+    if (!comm->allreduce_sum(rc, ndofs[l - 1], prec, stream)) return fail(IPMG_ERR_NCCL, comm->err);
+    return IPMG_OK;
+  }
   ipmg_status vcycle_level(int l, int prec) {
     void* b = vb[prec][l];
     void* const x0 = vx0[prec][l];
     void* const x1 = vx1[prec][l];
     if (l == 0) return coarse(prec, b, x1);
-    ipmg_status st;
+    ipmg_status st = halo(l, prec, b);   // straddling patches read b on the ghost cells
+    if (st != IPMG_OK) return st;
     const bool additive = cfg.smoother == IPMG_ADDITIVE;
     // (1) pre-smoothing from x = 0; smooth_* leave the result in their first buffer
     if (additive) st = smooth_add(l, prec, x1, x0, b, true);
     else st = smooth_mult(l, prec, x1, x0, b, false, true);
     if (st != IPMG_OK) return st;
     // (2) coarse-grid correction x1 += P P_{l-1}^{-1} P^T (b - A x1)
-    st = run(KC_RESTRICT, l, esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]), 1,
-             [&] { return ks.restrict_(dim, prec, x1, b, vb[prec][l - 1], geom[l], geom[l - 1], stream); }, "restrict");
+    st = halo(l, prec, x1);
+    if (st != IPMG_OK) return st;
+    st = restrict_to(l, prec, x1, b, vb[prec][l - 1]);
     if (st != IPMG_OK) return st;
     st = vcycle_level(l - 1, prec);
     if (st != IPMG_OK) return st;
@@ -325,11 +407,24 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
     ipmg_status st = h->cuda(h->ks.upload(h->fe), "table upload");
     if (st != IPMG_OK) return bail(st);
   }
-  // ---- hierarchy
+  // ---- hierarchy, slab partition of every level
+  h->comm = cfg->comm;
+  if (h->comm) {
+    h->rank = h->comm->rank;
+    h->nranks = h->comm->nranks;
+  }
   for (int l = 0; l < h->nlev; ++l) {
     ipmg::LevelGeom g{};
     g.n[2] = 1;
     for (int a = 0; a < h->dim; ++a) g.n[a] = cfg->coarse_cells[a] << l;
+    int part[4];
+    partition_rule(h->dim, cfg->coarse_cells, l, h->nranks, h->rank, part);
+    g.n[h->dim - 1] = part[2];
+    g.zoff = part[1];
+    g.nglob = part[3];
+    h->dist.push_back(part[0]);
+    const long long layer = h->dim == 2 ? g.n[0] : (long long)g.n[0] * g.n[1];
+    h->ghost.push_back(h->nranks > 1 && part[0] ? 2 * layer * h->cell : 0);
     g.grouped = l >= 1 ? 1 : 0;
     g.ncells = (long long)g.n[0] * g.n[1] * g.n[2];
     const double hh = cfg->h0 / double(1LL << l);
@@ -338,6 +433,10 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
     h->geom.push_back(g);
     h->ndofs.push_back(g.ncells * h->cell);
     h->hsize.push_back(hh);
+  }
+  if (h->nranks > 1 && !h->dist[h->nlev - 1]) {
+    h->err = "too many ranks: the finest level has fewer than 2 cell layers per rank along the slowest axis";
+    return bail(IPMG_ERR_INVALID_ARG);
   }
   // ---- coarse FD tables (global 1D eigenpairs on level 0)
   h->cdesc.dim = h->dim;
@@ -383,7 +482,8 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   }
   h->partial = (double*)h->dalloc(sizeof(double) * h->partial_len);
   h->scal = (double*)h->dalloc(sizeof(double) * 8);
-  if (!h->pattern || !h->partial || !h->scal) { h->err = "alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
+  h->gbuf = (double*)h->dalloc(sizeof(double) * 4 * h->nranks);
+  if (!h->pattern || !h->partial || !h->scal || !h->gbuf) { h->err = "alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
   {
     std::vector<double> pat((size_t)h->cell * h->nlev);
     for (int l = 0; l < h->nlev; ++l)
@@ -420,6 +520,69 @@ ipmg_status ipmg_destroy(ipmg_handle* h) {
   return IPMG_OK;
 }
 
+ipmg_status ipmg_partition(int dim, const int coarse_cells[3], int n_levels, int nranks, int rank, int level,
+                           int out[4]) {
+  if ((dim != 2 && dim != 3) || !coarse_cells || !out || n_levels < 1 || level < 0 || level >= n_levels ||
+      nranks < 1 || rank < 0 || rank >= nranks)
+    return IPMG_ERR_INVALID_ARG;
+  for (int a = 0; a < dim; ++a)
+    if (coarse_cells[a] != 1 && coarse_cells[a] != 2) return IPMG_ERR_INVALID_ARG;
+  partition_rule(dim, coarse_cells, level, nranks, rank, out);
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_level_partition(const ipmg_handle* h, int level, int* distributed, int* zoff, int* nglob) {
+  if (!h || level < 0 || level >= h->nlev) return IPMG_ERR_INVALID_ARG;
+  if (distributed) *distributed = h->dist[level];
+  if (zoff) *zoff = h->geom[level].zoff;
+  if (nglob) *nglob = h->geom[level].nglob;
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_nccl_unique_id(void* id128) {
+  if (!id128) return IPMG_ERR_INVALID_ARG;
+  std::string e;
+  if (!ipmg::nccl_unique_id(id128, &e)) {
+    g_create_error = e;
+    return IPMG_ERR_NCCL;
+  }
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_comm_create_nccl(const void* id128, int rank, int nranks, int device, ipmg_comm** out) {
+  if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks) return IPMG_ERR_INVALID_ARG;
+  std::string e;
+  *out = ipmg::make_nccl_comm(id128, rank, nranks, device, &e);
+  if (!*out) {
+    g_create_error = e;
+    return IPMG_ERR_NCCL;
+  }
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_comm_create_local(int nranks, const int* devices, ipmg_comm** out) {
+  if (!out || nranks < 1) return IPMG_ERR_INVALID_ARG;
+  auto team = std::make_shared<ipmg::Team>();
+  team->n = nranks;
+  team->slots.resize(nranks);
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  for (int r = 0; r < nranks; ++r) {
+    std::string e;
+    out[r] = ipmg::make_local_comm(team, r, devices ? devices[r] : 0, &e);
+    if (!out[r]) {
+      g_create_error = e;
+      for (int q = 0; q < r; ++q) delete out[q];
+      return IPMG_ERR_CUDA;
+    }
+  }
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_comm_destroy(ipmg_comm* c) {
+  delete c;
+  return IPMG_OK;
+}
+
 ipmg_status ipmg_level_info(const ipmg_handle* h, int level, int64_t* ndofs, int cells[3], double* hsize) {
   if (!h || level < 0 || level >= h->nlev) return IPMG_ERR_INVALID_ARG;
   if (ndofs) *ndofs = h->ndofs[level];
@@ -440,8 +603,11 @@ ipmg_status ipmg_vmult(ipmg_handle* h, int level, int precision, const void* x, 
     for (int a = 0; a < h->dim; ++a)
       if (h->geom[0].n[a] % 2) return h->fail(IPMG_ERR_UNSUPPORTED, "ipmg_vmult: level 0 with odd cell count");
   }
+  const void* xg = nullptr;
+  ipmg_status st = h->ghosted(level, precision, 0, x, &xg);
+  if (st != IPMG_OK) return st;
   return h->run(KC_VMULT, level, 2.0 * h->esize(precision) * h->ndofs[level], 1,
-                [&] { return h->ks.vmult(h->dim, precision, x, y, h->geom[level], nullptr, nullptr, nullptr, h->stream); },
+                [&] { return h->ks.vmult(h->dim, precision, xg, y, h->geom[level], nullptr, nullptr, nullptr, h->stream); },
                 "vmult");
 }
 
@@ -451,7 +617,12 @@ ipmg_status ipmg_smooth_colour(ipmg_handle* h, int level, int precision, const v
   if (level < 1 || level >= h->nlev || bad_prec(precision) || !b || !x_out || x_in == x_out || colour < 0 ||
       colour >= (1 << h->dim))
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_smooth_colour: bad arguments");
-  return h->smooth_colour(level, precision, x_in, b, x_out, colour);
+  const void *xg = nullptr, *bg = nullptr;
+  ipmg_status st = h->ghosted(level, precision, 0, x_in, &xg);
+  if (st != IPMG_OK) return st;
+  st = h->ghosted(level, precision, 1, b, &bg);
+  if (st != IPMG_OK) return st;
+  return h->smooth_colour(level, precision, xg, bg, x_out, colour);
 }
 
 ipmg_status ipmg_smooth(ipmg_handle* h, int level, int precision, void* x, const void* b, int reverse) {
@@ -460,6 +631,20 @@ ipmg_status ipmg_smooth(ipmg_handle* h, int level, int precision, void* x, const
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_smooth: bad arguments");
   ipmg_status st = h->ensure_scratch(precision, level);
   if (st != IPMG_OK) return st;
+  if (h->ghost[level] > 0) {   // distributed: run on ghosted copies, copy the result back
+    const void *xg = nullptr, *bg = nullptr;
+    st = h->ghosted(level, precision, 0, x, &xg);
+    if (st != IPMG_OK) return st;
+    st = h->ghosted(level, precision, 1, b, &bg);
+    if (st != IPMG_OK) return st;
+    void* xw = const_cast<void*>(xg);
+    st = h->cfg.smoother == IPMG_ADDITIVE ? h->smooth_add(level, precision, xw, h->scratch[precision][level], bg, false)
+                                          : h->smooth_mult(level, precision, xw, h->scratch[precision][level], bg,
+                                                           reverse != 0, false);
+    if (st != IPMG_OK) return st;
+    return h->cuda(cudaMemcpyAsync(x, xw, h->ndofs[level] * h->esize(precision), cudaMemcpyDeviceToDevice, h->stream),
+                   "copy back");
+  }
   if (h->cfg.smoother == IPMG_ADDITIVE) return h->smooth_add(level, precision, x, h->scratch[precision][level], b, false);
   return h->smooth_mult(level, precision, x, h->scratch[precision][level], b, reverse != 0, false);
 }
@@ -469,12 +654,10 @@ ipmg_status ipmg_residual_restrict(ipmg_handle* h, int fine_level, int precision
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !b || !r_c)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_residual_restrict: bad arguments");
-  return h->run(KC_RESTRICT, fine_level, h->esize(precision) * (2.0 * h->ndofs[fine_level] + h->ndofs[fine_level - 1]), 1,
-                [&] {
-                  return h->ks.restrict_(h->dim, precision, x, b, r_c, h->geom[fine_level], h->geom[fine_level - 1],
-                                         h->stream);
-                },
-                "restrict");
+  const void* xg = nullptr;
+  ipmg_status st = h->ghosted(fine_level, precision, 0, x, &xg);
+  if (st != IPMG_OK) return st;
+  return h->restrict_to(fine_level, precision, xg, b, r_c);
 }
 
 ipmg_status ipmg_prolongate_add(ipmg_handle* h, int fine_level, int precision, const void* e_c, void* x_f) {
@@ -535,9 +718,10 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
   const int L = h->nlev - 1;
   const long long n = h->ndofs[L];
   auto t0 = std::chrono::steady_clock::now();
+  if (h->comm) cudaSetDevice(h->cfg.device);
   if (!h->r) {
     h->r = (double*)h->dalloc(n * 8);
-    h->p = (double*)h->dalloc(n * 8);
+    h->p = (double*)h->valloc(L, IPMG_FP64);   // read with ghosts by the operator
     h->q = (double*)h->dalloc(n * 8);
     h->z = (double*)h->dalloc(n * 8);
     if (!h->r || !h->p || !h->q || !h->z) {
@@ -559,6 +743,7 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
   h->n_launches += 2;
   CK(ipmg::dot_partial(0, 0, h->r, h->r, n, h->partial, s), "dot");
   CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
+  if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
   CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
   CK(cudaStreamSynchronize(s), "sync");
   const double r0 = std::sqrt(h->hpin[0]);
@@ -585,24 +770,29 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       h->n_launches += 3;
       CK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), "dot");
       CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
+      if ((st = h->allsum(h->scal + cur)) != IPMG_OK) return st;
       CK(ipmg::cg_update_p32(h->p, z32, n, h->scal, cur, -1, s), "p = z");
     } else {
       st = h->vcycle(h->r, h->z, h->partial);
       if (st != IPMG_OK) return st;
       h->n_launches += 1;
       CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
+      if ((st = h->allsum(h->scal + cur)) != IPMG_OK) return st;
       CK(cudaMemcpyAsync(h->p, h->z, n * 8, cudaMemcpyDeviceToDevice, s), "copy p");
     }
     while (it < max_it) {
       long long nparts = 0;
+      if ((st = h->halo(L, IPMG_FP64, h->p)) != IPMG_OK) return st;
       st = h->run(KC_VMULT, L, 16.0 * n, 1,
                   [&] { return h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, h->partial, &nparts, s); },
                   "vmult");
       if (st != IPMG_OK) return st;
       h->n_launches += 3;
       CK(ipmg::finalize(h->partial, h->scal + 2, s, nparts), "finalize");
+      if ((st = h->allsum(h->scal + 2)) != IPMG_OK) return st;
       CK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s, r32), "update");
       CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
+      if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
       CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
       CK(cudaStreamSynchronize(s), "sync");
       ++it;
@@ -615,12 +805,14 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
         h->n_launches += 3;
         CK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), "dot");
         CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
+        if ((st = h->allsum(h->scal + (1 - cur))) != IPMG_OK) return st;
         CK(ipmg::cg_update_p32(h->p, z32, n, h->scal, 1 - cur, cur, s), "update p");
       } else {
         st = h->vcycle(h->r, h->z, h->partial);
         if (st != IPMG_OK) return st;
         h->n_launches += 2;
         CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
+        if ((st = h->allsum(h->scal + (1 - cur))) != IPMG_OK) return st;
         CK(ipmg::cg_update_p(h->p, h->z, n, h->scal, 1 - cur, cur, s), "update p");
       }
       cur = 1 - cur;

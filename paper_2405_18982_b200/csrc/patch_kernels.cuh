@@ -475,43 +475,63 @@ __device__ __forceinline__ int node_of_cell(int q, int l) {
 // ---------------------------------------------------------------- patch indexing
 template <int D>
 struct PInfo {
-  long long coff[1 << D];                 // element offset of every patch cell
-  long long nb[2 * D][1 << (D - 1)];      // neighbour cell across face (a, side), -1: none
-  int var[3];                             // boundary variant per direction
+  long long coff[1 << D];                 // element offset of every patch cell (ghost cells: outside 0..n)
+  long long nb[2 * D][1 << (D - 1)];      // neighbour cell across face (a, side), NO_NB: none
+  int var[3];                             // boundary variant per direction (global position)
   int valid;
-  int c0[3];
+  int own;                                // bit s: the cells with slowest-axis bit s are local (written)
+  int c0[3];                              // lowest patch cell, local coordinates
 };
+
+// patches of a colour along the slowest axis S of a slab:
+// unshifted: local lowest cells 0, 2, .., n-2; shifted: -1, 1, .., n-1 without
+// the ones that would leave the global domain (-1 at zoff = 0, n-1 at the top)
+__host__ __device__ inline int slab_patches(const LevelGeom& g, int S, int shifted) {
+  if (!shifted) return g.n[S] / 2;
+  return g.n[S] / 2 + 1 - (g.zoff == 0 ? 1 : 0) - (g.zoff + g.n[S] == g.nglob ? 1 : 0);
+}
+__host__ __device__ inline int slab_first(const LevelGeom& g, int shifted) {
+  return shifted ? (g.zoff == 0 ? 1 : -1) : 0;
+}
 
 __host__ __device__ inline long long num_patches(const LevelGeom& g, int dim, int colour) {
   long long np = 1;
-  for (int a = 0; a < dim; ++a) np *= (g.n[a] / 2 - ((colour >> a) & 1));
-  return np;
+  for (int a = 0; a < dim - 1; ++a) np *= (g.n[a] / 2 - ((colour >> a) & 1));
+  return np * slab_patches(g, dim - 1, (colour >> (dim - 1)) & 1);
 }
 
 // fills PInfo of the CTA's patches; one thread per (patch, item).  The grid is
 // (x-blocks of PPC patches, patch row j1, patch plane j2) of the colour's patch
-// lattice, so patch coordinates need no division.
+// lattice, so patch coordinates need no division.  Boundary variants and
+// neighbour existence along the slowest axis use GLOBAL coordinates; patches
+// straddling the slab boundary (shifted colours) are computed by both ranks,
+// each writing only its own cells (`own`).
 template <int D, typename T>
 __device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g, int colour) {
   using C = Cfg<D, T>;
+  constexpr int S = D - 1;
   constexpr int ITEMS = 1 + C::NCH + C::NNB;
   const int m0 = g.n[0] / 2 - (colour & 1);
+  const int c0s = slab_first(g, (colour >> S) & 1) + 2 * (int)(D == 3 ? blockIdx.z : blockIdx.y);
   for (int e = threadIdx.x; e < C::PPC * ITEMS; e += blockDim.x) {
     const int p = e / ITEMS, it = e % ITEMS;
     const int j0 = blockIdx.x * C::PPC + p;
     const bool valid = j0 < m0;
     const int c0x = (colour & 1) + 2 * (valid ? j0 : 0);
-    const int c0y = ((colour >> 1) & 1) + 2 * (int)blockIdx.y;
-    const int c0z = (D == 3) ? ((colour >> 2) & 1) + 2 * (int)blockIdx.z : 0;
+    const int c0y = (D == 3) ? ((colour >> 1) & 1) + 2 * (int)blockIdx.y : c0s;
+    const int c0z = (D == 3) ? c0s : 0;
     PInfo<D>& pi = pis[p];
     if (it == 0) {
       pi.valid = valid;
       pi.c0[0] = c0x;
       pi.c0[1] = c0y;
       pi.c0[2] = c0z;
+      pi.own = (c0s >= 0 ? 1 : 0) | (c0s + 1 < g.n[S] ? 2 : 0);
+      const int gs = g.zoff + c0s;
+      const int vs = (gs == 0 ? 1 : 0) | (gs + 2 == g.nglob ? 2 : 0);
       pi.var[0] = (c0x == 0 ? 1 : 0) | (c0x + 2 == g.n[0] ? 2 : 0);
-      pi.var[1] = (c0y == 0 ? 1 : 0) | (c0y + 2 == g.n[1] ? 2 : 0);
-      pi.var[2] = (D == 3) ? ((c0z == 0 ? 1 : 0) | (c0z + 2 == g.n[2] ? 2 : 0)) : 0;
+      pi.var[1] = (D == 3) ? ((c0y == 0 ? 1 : 0) | (c0y + 2 == g.n[1] ? 2 : 0)) : vs;
+      pi.var[2] = (D == 3) ? vs : 0;
     } else if (it <= C::NCH) {
       const int q = it - 1;
       pi.coff[q] = cell_offset_cells(g, c0x + (q & 1), c0y + ((q >> 1) & 1), c0z + ((q >> 2) & 1)) * (long long)C::CELL;
@@ -526,8 +546,8 @@ __device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g,
       const int cy = c0y + (a == 1 ? sa : (a == 0 ? tb : tcb));
       const int cz = c0z + (D == 3 ? (a == 2 ? sa : tcb) : 0);
       const int ca = a == 0 ? cx : (a == 1 ? cy : cz);
-      const bool ex = valid && ca >= 0 && ca < g.n[a];
-      pi.nb[fs][t] = ex ? cell_offset_cells(g, cx, cy, cz) * (long long)C::CELL : -1LL;
+      const bool ex = valid && (a == S ? (g.zoff + ca >= 0 && g.zoff + ca < g.nglob) : (ca >= 0 && ca < (a == 0 ? g.n[0] : g.n[1])));   // a < S here
+      pi.nb[fs][t] = ex ? cell_offset_cells(g, cx, cy, cz) * (long long)C::CELL : NO_NB;
     }
   }
   __syncthreads();
@@ -680,7 +700,7 @@ __device__ __forceinline__ void stage_neighbors(T* NB, const T* __restrict__ x, 
   for (int e = threadIdx.x; e < npc * C::NNB * UPC; e += blockDim.x) {
     const int slot = e / UPC, c = e % UPC, p = slot / C::NNB, k = slot % C::NNB;
     const long long nb = pis[p].nb[k >> (D - 1)][k & ((1 << (D - 1)) - 1)];
-    if (nb >= 0) cp_async<C::CPB>(NB + slot * C::SP + c * EPC, x + nb + c * EPC);
+    if (nb != NO_NB) cp_async<C::CPB>(NB + slot * C::SP + c * EPC, x + nb + c * EPC);
   }
   cp_async_commit();
 }
@@ -725,7 +745,7 @@ __device__ __forceinline__ void trace_unit(T* F, const T* __restrict__ x, const 
   T u[NC], du[NC];
 #pragma unroll
   for (int i = 0; i < NC; ++i) u[i] = du[i] = T(0);
-  if (nb >= 0) {
+  if (nb != NO_NB) {
     // rows: A=0 -> row lb = x_{., lb, lc}; A=1 -> row j = x_{., j, lc}; A=2 -> row j = x_{., lc, j}
     const int lc = ic % NC;
     const int off = (D == 3 ? (A == 2 ? NC * lc : NC * NC * lc) : 0);
@@ -986,6 +1006,7 @@ __device__ __forceinline__ void store_rows(T* __restrict__ dst, const T* __restr
   for (int r = 0; r < R; ++r) {
     int qlo, r0;
     row_cells<D>(g + r * C::G, qlo, r0);
+    if (!((pi.own >> ((qlo >> (D - 1)) & 1)) & 1)) continue;   // ghost cells of a straddling patch
     store_seg<MODE, T, V>(dst + pi.coff[qlo] + r0, bm ? bm + pi.coff[qlo] + r0 : nullptr, scale, &v[r][0]);
     store_seg<MODE, T, V>(dst + pi.coff[qlo + 1] + r0, bm ? bm + pi.coff[qlo + 1] + r0 : nullptr, scale, &v[r][NC]);
   }
@@ -1248,11 +1269,15 @@ __global__ void copy_uncovered_kernel(const T* __restrict__ x_in, T* __restrict_
     if (!((colour >> a) & 1)) continue;
     long long layer = 1;
     for (int bb = 0; bb < D; ++bb) if (bb != a) layer *= g.n[bb];
-    const long long total = 2 * layer * C::CELL;
+    // slowest axis of a slab: only the layers on the global domain boundary are uncovered
+    const int s_first = (a == D - 1 && g.zoff != 0) ? 1 : 0;
+    const int s_last = (a == D - 1 && g.zoff + g.n[a] != g.nglob) ? 0 : 1;
+    if (s_last < s_first) continue;
+    const long long total = (s_last - s_first + 1) * layer * C::CELL;
     for (long long e = idx; e < total; e += stride_all) {
       const long long cell = e / C::CELL;
       const int l = (int)(e % C::CELL);
-      const int side = (int)(cell / layer);
+      const int side = s_first + (int)(cell / layer);
       long long rem = cell % layer;
       int cc[3] = {0, 0, 0};
       for (int bb = 0; bb < D; ++bb) {
@@ -1318,6 +1343,17 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) additive_kernel(const T* __rest
   fd_post<D, false>(X, X, pis, C::PPC, [&](int p, int gg, const T (&w)[C::R][NP]) {
     store_rows<D, 1, C::R>(x, (const T*)nullptr, pis[p], gg, omega, w);
   });
+}
+
+// parent (coarse) cell of the colour-0 patch with lowest fine cell c0 (local):
+// along the slowest axis through the global index, so that a replicated coarse
+// level (gc.zoff = 0, full size) and a distributed one (gc.zoff = gf.zoff / 2)
+// are both addressed correctly
+template <int D>
+__device__ __forceinline__ long long coarse_cell(const LevelGeom& gf, const LevelGeom& gc, const int (&c0)[3]) {
+  constexpr int S = D - 1;
+  const int cs = ((gf.zoff + c0[S]) >> 1) - gc.zoff;
+  return D == 3 ? cell_offset_cells(gc, c0[0] >> 1, c0[1] >> 1, cs) : cell_offset_cells(gc, c0[0] >> 1, cs, 0);
 }
 
 template <typename T>
@@ -1398,8 +1434,7 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) restrict_kernel(const T* __rest
     const int p = e / C::CELL, l = e % C::CELL;
     if (!pis[p].valid) continue;
     const PInfo<D>& pi = pis[p];
-    const long long o =
-        cell_offset_cells(gc, pi.c0[0] >> 1, pi.c0[1] >> 1, D == 3 ? pi.c0[2] >> 1 : 0) * C::CELL + l;
+    const long long o = coarse_cell<D>(gf, gc, pi.c0) * C::CELL + l;
     rc[o] = X[p * C::TSZ + node_of_cell<D, T>(0, l)];
   }
 }
@@ -1418,7 +1453,7 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) prolong_kernel(const T* __restr
     const PInfo<D>& pi = pis[p];
     T v = T(0);
     if (pi.valid)
-      v = __ldg(ec + cell_offset_cells(gc, pi.c0[0] >> 1, pi.c0[1] >> 1, D == 3 ? pi.c0[2] >> 1 : 0) * C::CELL + l);
+      v = __ldg(ec + coarse_cell<D>(gf, gc, pi.c0) * C::CELL + l);
     X[p * C::TSZ + node_of_cell<D, T>(0, l)] = v;
   }
   __syncthreads();
@@ -1466,8 +1501,9 @@ inline cudaError_t set_smem(F* f, size_t bytes) {
 template <int D, typename T>
 inline dim3 patch_grid(const LevelGeom& g, int colour) {
   using C = Cfg<D, T>;
-  const int m0 = g.n[0] / 2 - (colour & 1), m1 = g.n[1] / 2 - ((colour >> 1) & 1);
-  const int m2 = (D == 3) ? g.n[2] / 2 - ((colour >> 2) & 1) : 1;
+  const int m0 = g.n[0] / 2 - (colour & 1);
+  const int m1 = (D == 3) ? g.n[1] / 2 - ((colour >> 1) & 1) : slab_patches(g, 1, (colour >> 1) & 1);
+  const int m2 = (D == 3) ? slab_patches(g, 2, (colour >> 2) & 1) : 1;
   return dim3((unsigned)((m0 + C::PPC - 1) / C::PPC), (unsigned)(m1 > 0 ? m1 : 0), (unsigned)(m2 > 0 ? m2 : 0));
 }
 

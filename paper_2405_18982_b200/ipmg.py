@@ -25,7 +25,8 @@ EXPORTS = ["ipmg_config_default", "ipmg_create", "ipmg_destroy", "ipmg_level_inf
            "ipmg_smooth", "ipmg_smooth_colour", "ipmg_residual_restrict", "ipmg_prolongate_add",
            "ipmg_coarse_solve", "ipmg_vcycle", "ipmg_cg_solve", "ipmg_rhs", "ipmg_to_cellwise",
            "ipmg_from_cellwise", "ipmg_synchronize", "ipmg_last_error", "ipmg_tables_1d",
-           "ipmg_profile", "ipmg_profile_read", "ipmg_launch_count"]
+           "ipmg_profile", "ipmg_profile_read", "ipmg_launch_count", "ipmg_level_partition", "ipmg_partition",
+           "ipmg_nccl_unique_id", "ipmg_comm_create_nccl", "ipmg_comm_create_local", "ipmg_comm_destroy"]
 
 KERNEL_CLASSES = {"smooth": 0, "vmult": 1, "restrict": 2, "prolong": 3, "coarse": 4, "blas": 5, "additive": 6}
 
@@ -36,7 +37,7 @@ class Config(ctypes.Structure):
                 ("smoother", ctypes.c_int), ("additive_omega", ctypes.c_double),
                 ("post_smooth_reverse", ctypes.c_int), ("vcycle_precision", ctypes.c_int),
                 ("penalty_scale", ctypes.c_double), ("device", ctypes.c_int),
-                ("cuda_stream", ctypes.c_void_p)]
+                ("cuda_stream", ctypes.c_void_p), ("comm", ctypes.c_void_p)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -81,6 +82,13 @@ def load():
         "ipmg_profile_read": (i, [vp, i, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]),
         "ipmg_launch_count": (i, [vp, ctypes.POINTER(ctypes.c_int64)]),
+        "ipmg_level_partition": (i, [vp, i, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_int)]),
+        "ipmg_partition": (i, [i, ctypes.c_int * 3, i, i, i, i, ctypes.c_int * 4]),
+        "ipmg_nccl_unique_id": (i, [ctypes.c_char_p]),
+        "ipmg_comm_create_nccl": (i, [ctypes.c_char_p, i, i, i, ctypes.POINTER(vp)]),
+        "ipmg_comm_create_local": (i, [i, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)]),
+        "ipmg_comm_destroy": (i, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -107,6 +115,69 @@ def tables_1d(k, what, penalty_scale=1.0):
     return np.array(buf[:n.value])
 
 
+def partition(dim, coarse_cells, n_levels, nranks, rank, level):
+    """Host-only slab partition rule (ipmg_partition): (distributed, zoff, local_layers, global_layers)."""
+    lib = load()
+    cc = (ctypes.c_int * 3)(*(list(coarse_cells) + [1] * (3 - len(coarse_cells))))
+    out = (ctypes.c_int * 4)()
+    st = lib.ipmg_partition(dim, cc, n_levels, nranks, rank, level, out)
+    if st != IPMG_OK:
+        raise IpmgError(st, "ipmg_partition")
+    return tuple(out)
+
+
+class Comm:
+    """A rank's communicator of the slab decomposition (ipmg_comm_*)."""
+
+    def __init__(self, ptr, rank, nranks, kind):
+        self.ptr, self.rank, self.nranks, self.kind = ptr, rank, nranks, kind
+
+    @staticmethod
+    def nccl_unique_id():
+        lib = load()
+        buf = ctypes.create_string_buffer(128)
+        st = lib.ipmg_nccl_unique_id(buf)
+        if st != IPMG_OK:
+            raise IpmgError(st, lib.ipmg_last_error(None).decode())
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, rank, nranks, device, unique_id):
+        """unique_id: the 128 bytes rank 0 got from nccl_unique_id(), broadcast to all ranks."""
+        lib = load()
+        c = ctypes.c_void_p()
+        st = lib.ipmg_comm_create_nccl(unique_id, rank, nranks, device, ctypes.byref(c))
+        if st != IPMG_OK:
+            raise IpmgError(st, lib.ipmg_last_error(None).decode())
+        return cls(c, rank, nranks, "nccl")
+
+    @classmethod
+    def from_torch_distributed(cls, device):
+        """NCCL communicator over the default torch.distributed process group
+        (the unique id travels through the group, gloo or nccl)."""
+        import torch.distributed as dist
+        rank, n = dist.get_rank(), dist.get_world_size()
+        obj = [cls.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls.nccl(rank, n, device, obj[0])
+
+    @classmethod
+    def local_team(cls, nranks, devices=None):
+        """In-process team: one member per host thread (tests the distributed path on one GPU)."""
+        lib = load()
+        arr = (ctypes.c_void_p * nranks)()
+        devs = (ctypes.c_int * nranks)(*(devices or [0] * nranks))
+        st = lib.ipmg_comm_create_local(nranks, devs, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)))
+        if st != IPMG_OK:
+            raise IpmgError(st, lib.ipmg_last_error(None).decode())
+        return [cls(ctypes.c_void_p(arr[r]), r, nranks, "local") for r in range(nranks)]
+
+    def close(self):
+        if self.ptr:
+            load().ipmg_comm_destroy(self.ptr)
+            self.ptr = None
+
+
 def _ptr(t):
     if t is None:
         return None
@@ -118,7 +189,7 @@ class Handle:
 
     def __init__(self, dim, degree, n_levels, coarse_cells=None, h0=0.5, smoother=MULTIPLICATIVE,
                  additive_omega=0.0, post_smooth_reverse=1, vcycle_precision=FP32, penalty_scale=1.0,
-                 device=0, stream=None):
+                 device=0, stream=None, comm=None):
         import torch
         self.lib = load()
         cfg = Config()
@@ -134,6 +205,8 @@ class Handle:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
         cfg.cuda_stream = ctypes.c_void_p(stream.cuda_stream)
+        cfg.comm = comm.ptr if comm is not None else None
+        self.comm = comm
         self.cfg = cfg
         h = ctypes.c_void_p()
         st = self.lib.ipmg_create(ctypes.byref(cfg), ctypes.byref(h))
@@ -164,6 +237,13 @@ class Handle:
         self._check(self.lib.ipmg_level_info(self.h, level, ctypes.byref(n), cells, ctypes.byref(hs)),
                     "level_info")
         return n.value, tuple(cells), hs.value
+
+    def level_partition(self, level):
+        """(distributed, zoff, nglob) of a level on this rank."""
+        d, z, g = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+        self._check(self.lib.ipmg_level_partition(self.h, level, ctypes.byref(d), ctypes.byref(z), ctypes.byref(g)),
+                    "level_partition")
+        return d.value, z.value, g.value
 
     def ndofs(self, level):
         return self.level_info(level)[0]
