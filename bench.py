@@ -48,13 +48,17 @@ def measured_peaks():
 # ---------------------------------------------------------------- roofline model
 def smoother_flops_per_dof(dim, k):
     """Algorithmic flops of one full-kernel colour pass per dof (DESIGN.md
-    "Roofline"): fast diagonalisation 2d dense (2k+2)x(2k+2) contractions
-    (2 flops per FMA) plus the face coupling (trace value/derivative, tangential
-    mass, distribution), counted per patch and divided by the patch dofs."""
+    "Roofline"), for the algorithm the kernel runs: fast diagonalisation with
+    the even/odd factorised interior eigenbasis -- 2d line transforms of
+    np^(d-1) lines each costing np^2/2 FMAs (two (np/2)^2 halves) + np adds,
+    and one eigenvalue scaling per patch dof -- plus the face coupling (trace
+    value/derivative, tangential mass, S^T M transforms, injection), counted per
+    patch and divided by the patch dofs.  (The dense-eigenbasis model of
+    SURVEY.md 8(d), 2d np^2 FMAs per line, is twice the FD term.)"""
     nc, np_ = k + 1, 2 * (k + 1)
     patch = np_ ** dim
     nfp = np_ ** (dim - 1)
-    fd = 2 * dim * patch * 2 * np_
+    fd = 2 * dim * np_ ** (dim - 1) * (np_ * np_ + np_) + patch
     per_dir = 2 * nfp * 2 * nc + (dim - 1) * 2 * 2 * nfp * 2 * nc + nfp * np_ * 3
     return (fd + dim * per_dir) / patch
 
@@ -214,10 +218,16 @@ def run_ours(args, rank, ws, local):
     if ws > 1:
         import torch.distributed as dist
     wl = WORKLOAD
+    comm = ipmg.Comm.from_torch_distributed(local) if ws > 1 else None
     h = ipmg.Handle(wl["dim"], wl["degree"], wl["n_levels"], coarse_cells=wl["coarse"],
-                    vcycle_precision=ipmg.FP32, device=local)
+                    vcycle_precision=ipmg.FP32, device=local, comm=comm)
     L = wl["n_levels"] - 1
-    n = h.ndofs(L)
+    n = h.ndofs(L)                      # this rank's dofs (slab of the finest level)
+    n_glob = n
+    if dist:
+        t = torch.tensor([n], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        n_glob = int(t.item())
     b = torch.empty(n, dtype=torch.float64, device=dev)
     h.rhs(L, b)
     x = torch.empty_like(b)
@@ -256,7 +266,7 @@ def run_ours(args, rank, ws, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = ws * n / (ms_step * 1e-3) / 1e9
+    value = n_glob / (ms_step * 1e-3) / 1e9     # strong scaling: the whole problem per step
 
     # ---- components (separately timed, CUDA events): vmult fp64 and one smoother step fp32
     comp = {}
@@ -337,16 +347,17 @@ def run_ours(args, rank, ws, local):
                  "share_of_step": ms_s / ms if ms > 0 else None,
                  "per_class_ms_share": {c: (v[1] / ms if ms > 0 else None) for c, v in prof.items()}})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 CG / f32 V-cycle", "data": "synthetic (f=1 right-hand side)",
-            "config": {"workload": wl["name"] + ": " + wl["desc"], "dofs_per_gpu": n,
-                       "parallelism": "1 GPU" if ws == 1 else "independent replicas per GPU (slab decomposition pending)",
+            "config": {"workload": wl["name"] + ": " + wl["desc"], "dofs": n_glob, "dofs_rank0": n,
+                       "parallelism": "1 GPU" if ws == 1 else
+                       "slab decomposition along y over %d ranks (NCCL halo exchange + allgathered CG scalars)" % ws,
                        "l2": "inputs larger than L2 (537 MB fp64 vectors), no flush"},
             "time_to_solution_ms": ms_step, "cg_iterations": its[-1], "nu": res["nu"],
             "components": comp, "roofline": roof, "clocks": clk, "gpu_launches": launches,
-            "e2e": {"value": ws * n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-                    "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms}}
-    if not args.no_cpu_baseline:
+            "e2e": {"value": n_glob / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n_glob,
+                    "d2h_bytes_per_step": 8 * n_glob, "ms_per_step": e2e_ms}}
+    if not args.no_cpu_baseline and ws == 1:
         line["cpu_baseline"] = run_cpu_baseline()
     print(json.dumps(line), flush=True)
 

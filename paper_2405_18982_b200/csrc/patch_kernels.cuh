@@ -174,6 +174,18 @@ struct Cfg {
   static constexpr bool STAGE = false;   // measured: the occupancy loss outweighs the prefetch
 #endif
   static constexpr int CPB = (CELL * (int)sizeof(T)) % 16 == 0 ? 16 : ((CELL * (int)sizeof(T)) % 8 == 0 ? 8 : 4);
+  // minimum resident CTAs per SM requested from ptxas (register cap), per (dim, precision)
+#ifndef IPMG_SMOOTH_MINB_2F
+#define IPMG_SMOOTH_MINB_2F 0
+#endif
+#ifndef IPMG_SMOOTH_MINB_3F
+#define IPMG_SMOOTH_MINB_3F 0
+#endif
+#ifndef IPMG_VMULT_MINB_2D
+#define IPMG_VMULT_MINB_2D 0
+#endif
+  static constexpr int MINB_SMOOTH = sizeof(T) == 4 ? (D == 2 ? IPMG_SMOOTH_MINB_2F : IPMG_SMOOTH_MINB_3F) : 0;
+  static constexpr int MINB_VMULT = (sizeof(T) == 8 && D == 2) ? IPMG_VMULT_MINB_2D : 0;   // 0: no request
 };
 
 template <typename T>
@@ -500,32 +512,73 @@ __host__ __device__ inline long long num_patches(const LevelGeom& g, int dim, in
   return np * slab_patches(g, dim - 1, (colour >> (dim - 1)) & 1);
 }
 
-// fills PInfo of the CTA's patches; one thread per (patch, item).  The grid is
-// (x-blocks of PPC patches, patch row j1, patch plane j2) of the colour's patch
-// lattice, so patch coordinates need no division.  Boundary variants and
-// neighbour existence along the slowest axis use GLOBAL coordinates; patches
-// straddling the slab boundary (shifted colours) are computed by both ranks,
-// each writing only its own cells (`own`).
+// Patch lattice coordinates of a CTA ("block" (bx, by, bz) of the colour's
+// patch grid: x-blocks of PPC patches, patch row j1, patch plane j2) and the
+// item decomposition of its setup: item 0 = patch info, 1..NCH = patch cells,
+// then the NNB face-neighbour cells.  Boundary variants and neighbour existence
+// along the slowest axis use GLOBAL coordinates; patches straddling the slab
+// boundary (shifted colours) are computed by both ranks, each writing only its
+// own cells (`own`).
+template <int D>
+struct PatchPos {
+  int c0[3];
+  bool valid;
+};
 template <int D, typename T>
-__device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g, int colour) {
+__device__ __forceinline__ PatchPos<D> patch_pos(const LevelGeom& g, int colour, int bx, int by, int bz, int p) {
+  using C = Cfg<D, T>;
+  constexpr int S = D - 1;
+  PatchPos<D> pp;
+  const int m0 = g.n[0] / 2 - (colour & 1);
+  const int c0s = slab_first(g, (colour >> S) & 1) + 2 * (D == 3 ? bz : by);
+  const int j0 = bx * C::PPC + p;
+  pp.valid = j0 < m0;
+  pp.c0[0] = (colour & 1) + 2 * (pp.valid ? j0 : 0);
+  pp.c0[1] = (D == 3) ? ((colour >> 1) & 1) + 2 * by : c0s;
+  pp.c0[2] = (D == 3) ? c0s : 0;
+  return pp;
+}
+// element offset of cell item it >= 1 (patch cell or face neighbour), NO_NB if absent
+template <int D, typename T>
+__device__ __forceinline__ long long item_offset(const LevelGeom& g, const PatchPos<D>& pp, int it) {
+  using C = Cfg<D, T>;
+  constexpr int S = D - 1;
+  const int c0x = pp.c0[0], c0y = pp.c0[1], c0z = pp.c0[2];
+  if (it <= C::NCH) {
+    const int q = it - 1;
+    return cell_offset_cells(g, c0x + (q & 1), c0y + ((q >> 1) & 1), c0z + ((q >> 2) & 1)) * (long long)C::CELL;
+  }
+  const int k2 = it - 1 - C::NCH;                 // (a, side, t)
+  constexpr int PER = 1 << (D - 1);
+  const int fs = k2 / PER, t = k2 % PER, a = fs >> 1, s = fs & 1;
+  // neighbour across face (a, s): shift -1 / +2 along a; tangential bits of t
+  const int sa = s == 0 ? -1 : 2;
+  const int tb = t & 1, tcb = (t >> 1) & 1;
+  const int cx = c0x + (a == 0 ? sa : tb);
+  const int cy = c0y + (a == 1 ? sa : (a == 0 ? tb : tcb));
+  const int cz = c0z + (D == 3 ? (a == 2 ? sa : tcb) : 0);
+  const int ca = a == 0 ? cx : (a == 1 ? cy : cz);
+  const bool ex = pp.valid && (a == S ? (g.zoff + ca >= 0 && g.zoff + ca < g.nglob)
+                                      : (ca >= 0 && ca < (a == 0 ? g.n[0] : g.n[1])));   // a < S here
+  return ex ? cell_offset_cells(g, cx, cy, cz) * (long long)C::CELL : NO_NB;
+}
+
+// fills PInfo of the CTA's patches; one thread per (patch, item)
+template <int D, typename T>
+__device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g, int colour, int bx, int by, int bz) {
   using C = Cfg<D, T>;
   constexpr int S = D - 1;
   constexpr int ITEMS = 1 + C::NCH + C::NNB;
-  const int m0 = g.n[0] / 2 - (colour & 1);
-  const int c0s = slab_first(g, (colour >> S) & 1) + 2 * (int)(D == 3 ? blockIdx.z : blockIdx.y);
   for (int e = threadIdx.x; e < C::PPC * ITEMS; e += blockDim.x) {
     const int p = e / ITEMS, it = e % ITEMS;
-    const int j0 = blockIdx.x * C::PPC + p;
-    const bool valid = j0 < m0;
-    const int c0x = (colour & 1) + 2 * (valid ? j0 : 0);
-    const int c0y = (D == 3) ? ((colour >> 1) & 1) + 2 * (int)blockIdx.y : c0s;
-    const int c0z = (D == 3) ? c0s : 0;
+    const PatchPos<D> pp = patch_pos<D, T>(g, colour, bx, by, bz, p);
     PInfo<D>& pi = pis[p];
     if (it == 0) {
-      pi.valid = valid;
-      pi.c0[0] = c0x;
-      pi.c0[1] = c0y;
-      pi.c0[2] = c0z;
+      const int c0x = pp.c0[0], c0y = pp.c0[1], c0s = pp.c0[S];
+      pi.valid = pp.valid;
+      pi.c0[0] = pp.c0[0];
+      pi.c0[1] = pp.c0[1];
+      pi.c0[2] = pp.c0[2];
       pi.own = (c0s >= 0 ? 1 : 0) | (c0s + 1 < g.n[S] ? 2 : 0);
       const int gs = g.zoff + c0s;
       const int vs = (gs == 0 ? 1 : 0) | (gs + 2 == g.nglob ? 2 : 0);
@@ -533,24 +586,40 @@ __device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g,
       pi.var[1] = (D == 3) ? ((c0y == 0 ? 1 : 0) | (c0y + 2 == g.n[1] ? 2 : 0)) : vs;
       pi.var[2] = (D == 3) ? vs : 0;
     } else if (it <= C::NCH) {
-      const int q = it - 1;
-      pi.coff[q] = cell_offset_cells(g, c0x + (q & 1), c0y + ((q >> 1) & 1), c0z + ((q >> 2) & 1)) * (long long)C::CELL;
+      pi.coff[it - 1] = item_offset<D, T>(g, pp, it);
     } else {
-      const int k2 = it - 1 - C::NCH;                 // (a, side, t)
+      const int k2 = it - 1 - C::NCH;
       constexpr int PER = 1 << (D - 1);
-      const int fs = k2 / PER, t = k2 % PER, a = fs >> 1, s = fs & 1;
-      // neighbour across face (a, s): shift -1 / +2 along a; tangential bits of t
-      const int sa = s == 0 ? -1 : 2;
-      const int tb = t & 1, tcb = (t >> 1) & 1;
-      const int cx = c0x + (a == 0 ? sa : tb);
-      const int cy = c0y + (a == 1 ? sa : (a == 0 ? tb : tcb));
-      const int cz = c0z + (D == 3 ? (a == 2 ? sa : tcb) : 0);
-      const int ca = a == 0 ? cx : (a == 1 ? cy : cz);
-      const bool ex = valid && (a == S ? (g.zoff + ca >= 0 && g.zoff + ca < g.nglob) : (ca >= 0 && ca < (a == 0 ? g.n[0] : g.n[1])));   // a < S here
-      pi.nb[fs][t] = ex ? cell_offset_cells(g, cx, cy, cz) * (long long)C::CELL : NO_NB;
+      pi.nb[k2 / PER][k2 % PER] = item_offset<D, T>(g, pp, it);
     }
   }
   __syncthreads();
+}
+template <int D, typename T>
+__device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g, int colour) {
+  setup_patches<D, T>(pis, g, colour, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z);
+}
+
+// L2 prefetch of the patch cells of src (TMA bulk prefetch, one instruction per
+// cell; the range is widened to 16-byte granularity).  Issued right after the
+// setup so that the HBM reads of the patch's own rows overlap the face-trace
+// phase instead of following it (the kernels are long-scoreboard bound).
+#ifndef IPMG_PREFETCH
+#define IPMG_PREFETCH 0   // measured: -5% (2D k=7), neutral in 3D
+#endif
+template <int D, typename T>
+__device__ __forceinline__ void prefetch_cells(const T* src, const PInfo<D>* pis, int npc) {
+#if IPMG_PREFETCH
+  using C = Cfg<D, T>;
+  if (src == nullptr) return;
+  for (int e = threadIdx.x; e < npc * C::NCH; e += blockDim.x) {
+    const PInfo<D>& pi = pis[e / C::NCH];
+    if (!pi.valid) continue;
+    const unsigned long long a = (unsigned long long)(src + pi.coff[e % C::NCH]);
+    const unsigned long long a0 = a & ~15ull, a1 = (a + C::CELL * sizeof(T) + 15) & ~15ull;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- cooperative copies
@@ -1209,7 +1278,7 @@ __device__ __forceinline__ void my_rows(const T* __restrict__ src, const PInfo<D
 
 // y = hs * A x   or, with bminus != nullptr, y = bminus - hs * A x
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D, T>::NT) vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
+__global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_VMULT) vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                               const T* __restrict__ bminus, LevelGeom g,
                                                               double* __restrict__ dot_partial) {
   using C = Cfg<D, T>;
@@ -1220,6 +1289,7 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) vmult_kernel(const T* __restric
   T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
   __shared__ PInfo<D> pis[C::PPC];
   setup_patches<D, T>(pis, g, 0);
+  prefetch_cells<D>(x, pis, C::PPC);
   if (C::STAGE) stage_neighbors<D>(NB, x, pis, C::PPC);
   T xr[C::R][NP];
 #ifdef IPMG_ROWS_EARLY
@@ -1293,10 +1363,13 @@ __global__ void copy_uncovered_kernel(const T* __restrict__ x_in, T* __restrict_
 }
 
 // one colour of the multiplicative full-kernel smoother (replacement form):
-// x_out_j = A_jj^{-1} (b_j - C_j x_in) for every patch j of the colour
+// x_out_j = A_jj^{-1} (b_j - C_j x_in) for every patch j of the colour.
+// (Measured alternatives: a persistent grid of resident CTAs
+// with an L2 prefetch of the next block, cp.async staging of the neighbour
+// cells, loading the b rows before the traces -- all slower.)
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D, T>::NT) smooth_kernel(const T* __restrict__ x_in, const T* __restrict__ b,
-                                                               T* __restrict__ x_out, LevelGeom g, int colour) {
+__global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_SMOOTH)
+    smooth_kernel(const T* __restrict__ x_in, const T* __restrict__ b, T* __restrict__ x_out, LevelGeom g, int colour) {
   using C = Cfg<D, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
@@ -1304,6 +1377,7 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) smooth_kernel(const T* __restri
   T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
   __shared__ PInfo<D> pis[C::PPC];
   setup_patches<D, T>(pis, g, colour);
+  prefetch_cells<D>(b, pis, C::PPC);
   if (x_in != nullptr && C::STAGE) stage_neighbors<D>(NB, x_in, pis, C::PPC);   // lands during fd_pre
   T br[C::R][NP];
 #ifdef IPMG_ROWS_EARLY
@@ -1383,6 +1457,7 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) restrict_kernel(const T* __rest
   T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
   __shared__ PInfo<D> pis[C::PPC];
   setup_patches<D, T>(pis, gf, 0);
+  prefetch_cells<D>(b, pis, C::PPC);
   const T hs = T(gf.hs);
   if (x != nullptr) {
     if (C::STAGE) stage_neighbors<D>(NB, x, pis, C::PPC);
