@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -85,6 +86,10 @@ struct ipmg_handle {
   std::vector<long long> ghost;       // elements of one ghost parent layer (0: no ghosts)
   double* gbuf = nullptr;             // allgathered per-rank scalars
   std::vector<void*> gsc[2][3];       // ghosted copies of caller vectors (API calls), [prec][slot][level]
+  // ---- the finest-level V-cycle captured as a CUDA graph per precision
+  cudaGraphExec_t vgraph[2] = {nullptr, nullptr};
+  long long vgraph_launches[2] = {0, 0};
+  bool use_graphs = true;
   // ---- instrumentation: launch counter and (optional) CUDA-event timing of
   // the finest-level kernels, per kernel class (ipmg_profile*)
   long long n_launches = 0;
@@ -286,7 +291,7 @@ struct ipmg_handle {
     if (st != IPMG_OK) return st;
     st = restrict_to(l, prec, x1, b, vb[prec][l - 1]);
     if (st != IPMG_OK) return st;
-    st = vcycle_level(l - 1, prec);
+    st = l == nlev - 1 ? run_coarse_vcycle(prec) : vcycle_level(l - 1, prec);
     if (st != IPMG_OK) return st;
     st = run(KC_PROLONG, l, esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]), 1,
              [&] { return ks.prolong(dim, prec, vx1[prec][l - 1], x1, geom[l], geom[l - 1], stream); }, "prolong");
@@ -294,6 +299,43 @@ struct ipmg_handle {
     // (3) post-smoothing (colours reversed for a symmetric V-cycle, reading A7)
     if (additive) return smooth_add(l, prec, x1, x0, b, false);
     return smooth_mult(l, prec, x1, x0, b, cfg.post_smooth_reverse != 0, false);
+  }
+  // The coarse part of the V-cycle (levels L-1 .. 0, launch-latency bound:
+  // ~100 small kernels) replayed from a CUDA graph captured on first use; the
+  // finest level's kernels are launched directly (so ipmg_profile still times
+  // them).  Not with a communicator that cannot be captured (in-process team).
+  ipmg_status run_coarse_vcycle(int prec) {
+    const int L = nlev - 2;
+    if (!use_graphs || (comm && !comm->capturable())) return vcycle_level(L, prec);
+    if (!vgraph[prec]) {
+      cudaStream_t cap = nullptr;
+      ipmg_status st = cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+      if (st != IPMG_OK) return st;
+      cudaStream_t saved = stream;
+      stream = cap;
+      const long long n0 = n_launches;
+      cudaGraph_t gph = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        st = vcycle_level(L, prec);
+        e = cudaStreamEndCapture(cap, &gph);
+      }
+      stream = saved;
+      if (e == cudaSuccess && st == IPMG_OK) e = cudaGraphInstantiate(&vgraph[prec], gph, 0);
+      if (gph) cudaGraphDestroy(gph);
+      cudaStreamDestroy(cap);
+      vgraph_launches[prec] = n_launches - n0;
+      n_launches = n0;
+      if (st != IPMG_OK) return st;
+      if (e != cudaSuccess) {   // capture unsupported here: fall back to direct launches from now on
+        vgraph[prec] = nullptr;
+        use_graphs = false;
+        cudaGetLastError();
+        return vcycle_level(L, prec);
+      }
+    }
+    n_launches += vgraph_launches[prec];
+    return cuda(cudaGraphLaunch(vgraph[prec], stream), "graph launch");
   }
   ipmg_status vcycle(const double* r, double* z, double* rz_partial) {
     const int prec = cfg.vcycle_precision;
@@ -390,6 +432,10 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   h->cell = h->dim == 2 ? h->nc * h->nc : h->nc * h->nc * h->nc;
   h->nlev = cfg->n_levels;
   h->stream = (cudaStream_t)cfg->cuda_stream;
+  {
+    const char* ng = std::getenv("IPMG_NO_GRAPH");
+    h->use_graphs = !(ng && ng[0] == '1');
+  }
   auto bail = [&](ipmg_status st) {
     g_create_error = h->err;
     ipmg_destroy(h);
@@ -510,6 +556,8 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
 
 ipmg_status ipmg_destroy(ipmg_handle* h) {
   if (!h) return IPMG_OK;
+  for (int p = 0; p < 2; ++p)
+    if (h->vgraph[p]) cudaGraphExecDestroy(h->vgraph[p]);
   for (auto& e : h->ev_pool) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);

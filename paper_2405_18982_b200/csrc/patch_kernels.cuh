@@ -29,6 +29,9 @@
 #include "fe1d.hpp"
 
 #include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #ifndef IPMG_K
 #error "IPMG_K must be defined by the including translation unit"
@@ -99,7 +102,11 @@ struct Cfg {
 #ifndef IPMG_GROUPS_TARGET
 #define IPMG_GROUPS_TARGET 32
 #endif
-  static constexpr int PPC = (IPMG_GROUPS_TARGET / G) > 1 ? (IPMG_GROUPS_TARGET / G) : 1;   // patches per CTA
+  // line groups per CTA: 1 warp (measured best for k >= 3); 4 warps for k <= 2,
+  // whose tiny patches otherwise leave a CTA with too little work (C3 sweep: 3D
+  // k=2 smoother step 10.4 -> 12.7 GDoF/s)
+  static constexpr int GT = NC <= 3 ? 4 * IPMG_GROUPS_TARGET : IPMG_GROUPS_TARGET;
+  static constexpr int PPC = (GT / G) > 1 ? (GT / G) : 1;   // patches per CTA
   static constexpr int GROUPS = PPC * G;
   static constexpr int NT = (((GROUPS + 31) / 32) * 32) > 256 ? 256 : ((GROUPS + 31) / 32) * 32;
 
@@ -1331,35 +1338,40 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_VMULT) vmult_ke
 // cells a shifted colour does not cover (boundary layers c_a in {0, n_a-1} of
 // every shifted direction a) are copied x_out = x_in (zero if x_in == nullptr)
 template <int D, typename T>
-__global__ void copy_uncovered_kernel(const T* __restrict__ x_in, T* __restrict__ x_out, LevelGeom g, int colour) {
+__device__ __forceinline__ void copy_uncovered_part(const T* __restrict__ x_in, T* __restrict__ x_out, const LevelGeom& g,
+                                                    int colour, long long idx0, long long stride0) {
   using C = Cfg<D, T>;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long stride_all = (long long)gridDim.x * blockDim.x;
+  // 32-bit index math (a boundary layer pair has < 2^31 values)
+  const unsigned idx = (unsigned)idx0, stride_all = (unsigned)stride0;
+#pragma unroll 1
   for (int a = 0; a < D; ++a) {
     if (!((colour >> a) & 1)) continue;
-    long long layer = 1;
-    for (int bb = 0; bb < D; ++bb) if (bb != a) layer *= g.n[bb];
+    // the other directions b0 < b1 (b1 only in 3D)
+    const unsigned n0 = (unsigned)(a == 0 ? g.n[1] : g.n[0]), n1 = D == 3 ? (unsigned)(a == 2 ? g.n[1] : g.n[2]) : 1u;
+    const unsigned layer = n0 * n1;
     // slowest axis of a slab: only the layers on the global domain boundary are uncovered
     const int s_first = (a == D - 1 && g.zoff != 0) ? 1 : 0;
-    const int s_last = (a == D - 1 && g.zoff + g.n[a] != g.nglob) ? 0 : 1;
+    const int s_last = (a == D - 1 && g.zoff + g.n[D - 1] != g.nglob) ? 0 : 1;
     if (s_last < s_first) continue;
-    const long long total = (s_last - s_first + 1) * layer * C::CELL;
-    for (long long e = idx; e < total; e += stride_all) {
-      const long long cell = e / C::CELL;
-      const int l = (int)(e % C::CELL);
-      const int side = s_first + (int)(cell / layer);
-      long long rem = cell % layer;
-      int cc[3] = {0, 0, 0};
-      for (int bb = 0; bb < D; ++bb) {
-        if (bb == a) continue;
-        cc[bb] = (int)(rem % g.n[bb]);
-        rem /= g.n[bb];
-      }
-      cc[a] = side ? g.n[a] - 1 : 0;
-      const long long o = cell_offset_cells(g, cc[0], cc[1], cc[2]) * C::CELL + l;
+    const unsigned total = (unsigned)(s_last - s_first + 1) * layer * (unsigned)C::CELL;
+    for (unsigned e = idx; e < total; e += stride_all) {
+      const unsigned cell = e / (unsigned)C::CELL, l = e % (unsigned)C::CELL;
+      const unsigned side = (unsigned)s_first + cell / layer, rem = cell % layer;
+      const int na = a == 0 ? g.n[0] : (a == 1 ? g.n[1] : g.n[2]);
+      const int ca = side ? na - 1 : 0, u = (int)(rem % n0), v = D == 3 ? (int)(rem / n0) : 0;
+      // (a, b0, b1) = (0, 1, 2), (1, 0, 2), (2, 0, 1)
+      const int cx = a == 0 ? ca : u;
+      const int cy = a == 1 ? ca : (a == 0 ? u : v);
+      const int cz = D == 3 ? (a == 2 ? ca : v) : 0;
+      const long long o = cell_offset_cells(g, cx, cy, cz) * C::CELL + l;
       x_out[o] = x_in ? __ldg(x_in + o) : T(0);
     }
   }
+}
+template <int D, typename T>
+__global__ void copy_uncovered_kernel(const T* __restrict__ x_in, T* __restrict__ x_out, LevelGeom g, int colour) {
+  copy_uncovered_part<D, T>(x_in, x_out, g, colour, (long long)blockIdx.x * blockDim.x + threadIdx.x,
+                            (long long)gridDim.x * blockDim.x);
 }
 
 // one colour of the multiplicative full-kernel smoother (replacement form):
@@ -1369,8 +1381,15 @@ __global__ void copy_uncovered_kernel(const T* __restrict__ x_in, T* __restrict_
 // cells, loading the b rows before the traces -- all slower.)
 template <int D, typename T>
 __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_SMOOTH)
-    smooth_kernel(const T* __restrict__ x_in, const T* __restrict__ b, T* __restrict__ x_out, LevelGeom g, int colour) {
+    smooth_kernel(const T* __restrict__ x_in, const T* __restrict__ b, T* __restrict__ x_out, LevelGeom g, int colour,
+                  int nbx) {
   using C = Cfg<D, T>;
+  if ((int)blockIdx.x >= nbx) {   // the extra column of CTAs copies the cells the colour does not cover
+    const long long q = blockIdx.y + (long long)gridDim.y * blockIdx.z;
+    copy_uncovered_part<D, T>(x_in, x_out, g, colour, q * blockDim.x + threadIdx.x,
+                              (long long)gridDim.y * gridDim.z * blockDim.x);
+    return;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* F = X + C::PPC * C::TSZ;
@@ -1567,9 +1586,21 @@ constexpr size_t smem_bytes(int ntensors, bool faces) {
                       (faces ? (size_t)C::PPC * C::FSZ + (C::STAGE ? (size_t)C::NBS : 0) : 0));
 }
 
+// cudaFuncSetAttribute once per (kernel, device, size): it is a host API call
+// that would otherwise be paid on every launch of the V-cycle
 template <typename F>
 inline cudaError_t set_smem(F* f, size_t bytes) {
-  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, long long>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const long long key = ((long long)dev << 40) | (long long)bytes;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == (const void*)f && d.second == key) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.emplace_back((const void*)f, key);
+  return e;
 }
 
 // grid over the colour's patch lattice: (x-blocks of PPC patches, j1, j2)
@@ -1606,11 +1637,12 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
   cudaError_t e = set_smem(smooth_kernel<D, T>, smem_bytes<D, T>(1, true));
   if (e != cudaSuccess) return e;
   if (grid.x * grid.y * grid.z > 0) {
-    smooth_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    // shifted colours: one extra column of CTAs copies the uncovered boundary layers
+    const dim3 g2(grid.x + (colour != 0 ? 1 : 0), grid.y, grid.z);
+    smooth_kernel<D, T><<<g2, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour, (int)grid.x);
+    return cudaGetLastError();
   }
-  if (colour != 0) {
+  if (colour != 0) {   // empty patch lattice (tiny level): copy only
     long long cells = 0;
     for (int a = 0; a < D; ++a) {
       if (!((colour >> a) & 1)) continue;
