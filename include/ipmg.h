@@ -188,6 +188,19 @@ ipmg_status ipmg_vcycle(ipmg_handle *h, const double *r, double *z);
 ipmg_status ipmg_cg_solve(ipmg_handle *h, const double *b, double *x, double rtol, int max_it,
                           ipmg_solve_info *info);
 
+/* Right-preconditioned GMRES without restart, modified Gram-Schmidt (the
+ * paper's outer solver),
+ * with the V-cycle of cfg (fp32 = mixed precision) as the preconditioner and the
+ * solution assembled as x = sum_i y_i P^{-1} v_i.  x_0 = 0; stops when the
+ * least-squares residual estimate |g_{j+1}| <= rtol ||b||_2.  history =
+ * ||b||, |g_1|, .., |g_n| (host); nu = -8 n / log10(|g_n| / ||b||) is the
+ * fractional iteration count of PAPER.md Tables 1/2/4.  b, x: double device
+ * vectors of the finest level; max_it <= 1000 (the Krylov basis, 2 max_it
+ * vectors, is library-owned and kept for later solves).  Returns
+ * IPMG_ERR_NOT_CONVERGED (info filled) when max_it is reached. */
+ipmg_status ipmg_gmres_solve(ipmg_handle *h, const double *b, double *x, double rtol, int max_it,
+                             ipmg_solve_info *info);
+
 /* Right-hand side b_i = int f phi_i on level `level` for f == 1;
  * kind must be 0.  b: double device vector of that level. */
 ipmg_status ipmg_rhs(ipmg_handle *h, int level, int kind, double *b);

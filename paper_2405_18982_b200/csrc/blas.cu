@@ -98,6 +98,47 @@ __global__ void __launch_bounds__(RED_THREADS) cast_dot_kernel(const float* __re
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
+// ---- GMRES (modified Gram-Schmidt, right preconditioning)
+// w -= h[ih] * v ; partial of w . u (u == nullptr: w . w) -- one MGS step fused
+// with the dot product of the next step
+__global__ void __launch_bounds__(RED_THREADS) mgs_axpy_dot_kernel(double* __restrict__ w, const double* __restrict__ v,
+                                                                    const double* __restrict__ u, long long n,
+                                                                    const double* __restrict__ h, int ih,
+                                                                    double* __restrict__ partial) {
+  __shared__ double sh[32];
+  const double c = h[ih];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double wi = fma(-c, v[i], w[i]);
+    w[i] = wi;
+    s = fma(wi, u ? u[i] : wi, s);
+  }
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// v = w / sqrt(nrm2[0]) ; v32 = (float) v (the next V-cycle input) when v32 != nullptr;
+// nrm2 == nullptr: v = w * scale
+__global__ void scale_kernel(double* __restrict__ v, const double* __restrict__ w, long long n,
+                             const double* __restrict__ nrm2, double scale, float* __restrict__ v32) {
+  const double f = nrm2 ? 1.0 / sqrt(nrm2[0]) : scale;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double vi = w[i] * f;
+    v[i] = vi;
+    if (v32) v32[i] = (float)vi;
+  }
+}
+
+// x = sum_i y[i] Z[i] (i < m), fixed order
+__global__ void combine_kernel(double* __restrict__ x, const double* const* __restrict__ Z, const double* __restrict__ y,
+                               int m, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < m; ++j) s = fma(y[j], Z[j][i], s);
+    x[i] = s;
+  }
+}
+
 template <typename TI, typename TO>
 __global__ void cast_kernel(const TI* __restrict__ in, TO* __restrict__ out, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -298,6 +339,23 @@ cudaError_t sum_ranks(int prec, void* buf, const void* scratch, int nranks, int 
 
 cudaError_t gather_sum(const double* g, int nranks, int nv, double* out, cudaStream_t s) {
   gather_sum_kernel<<<1, 32, 0, s>>>(g, nranks, nv, out);
+  return cudaGetLastError();
+}
+
+cudaError_t mgs_axpy_dot(double* w, const double* v, const double* u, long long n, const double* h, int ih,
+                         double* partial, cudaStream_t s) {
+  mgs_axpy_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(w, v, u, n, h, ih, partial);
+  return cudaGetLastError();
+}
+
+cudaError_t scale_vec(double* v, const double* w, long long n, const double* nrm2, double scale, float* v32,
+                      cudaStream_t s) {
+  scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, w, n, nrm2, scale, v32);
+  return cudaGetLastError();
+}
+
+cudaError_t combine(double* x, const double* const* Z, const double* y, int m, long long n, cudaStream_t s) {
+  combine_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, Z, y, m, n);
   return cudaGetLastError();
 }
 

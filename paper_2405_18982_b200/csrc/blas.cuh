@@ -30,6 +30,11 @@ cudaError_t permute(int prec, bool to_cellwise, const void* in, void* out, const
                     cudaStream_t s);
 cudaError_t sum_ranks(int prec, void* buf, const void* scratch, int nranks, int rank, long long n, cudaStream_t s);
 cudaError_t gather_sum(const double* g, int nranks, int nv, double* out, cudaStream_t s);
+cudaError_t mgs_axpy_dot(double* w, const double* v, const double* u, long long n, const double* h, int ih,
+                         double* partial, cudaStream_t s);
+cudaError_t scale_vec(double* v, const double* w, long long n, const double* nrm2, double scale, float* v32,
+                      cudaStream_t s);
+cudaError_t combine(double* x, const double* const* Z, const double* y, int m, long long n, cudaStream_t s);
 cudaError_t pattern_fill(double* b, const double* pat, int cell, long long n, cudaStream_t s);
 cudaError_t coarse_solve(int prec, const void* b, void* x, const CoarseDesc& cd, const void* const S[3],
                          const void* const L[3], cudaStream_t s);

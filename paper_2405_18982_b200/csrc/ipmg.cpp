@@ -87,6 +87,11 @@ struct ipmg_handle {
   double* gbuf = nullptr;             // allgathered per-rank scalars
   std::vector<void*> gsc[2][3];       // ghosted copies of caller vectors (API calls), [prec][slot][level]
   // ---- the finest-level V-cycle captured as a CUDA graph per precision
+  // ---- GMRES workspace (finest level, fp64): Krylov basis V, preconditioned Z
+  std::vector<double*> gV, gZ;
+  double *gw = nullptr, *ghcol = nullptr, *gy = nullptr, *ghpin = nullptr;
+  const double** gzptr = nullptr;
+  int gcap = 0;
   cudaGraphExec_t vgraph[2] = {nullptr, nullptr};
   long long vgraph_launches[2] = {0, 0};
   bool use_graphs = true;
@@ -564,6 +569,7 @@ ipmg_status ipmg_destroy(ipmg_handle* h) {
   }
   for (void* p : h->allocs) cudaFree(p);
   if (h->hpin) cudaFreeHost(h->hpin);
+  if (h->ghpin) cudaFreeHost(h->ghpin);
   delete h;
   return IPMG_OK;
 }
@@ -881,6 +887,158 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     }
   }
   if (!conv) return h->fail(IPMG_ERR_NOT_CONVERGED, "ipmg_cg_solve: max_it reached");
+  return IPMG_OK;
+}
+
+ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double rtol, int max_it,
+                             ipmg_solve_info* info) {
+  if (!h) return IPMG_ERR_INVALID_ARG;
+  if (!b || !x || (const void*)b == (const void*)x || !(rtol > 0) || max_it < 1 || max_it > 1000)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_gmres_solve: bad arguments");
+  const int L = h->nlev - 1;
+  const long long n = h->ndofs[L];
+  auto t0 = std::chrono::steady_clock::now();
+  if (h->comm) cudaSetDevice(h->cfg.device);
+  cudaStream_t s = h->stream;
+  const bool mixed = h->cfg.vcycle_precision == IPMG_FP32;
+  ipmg_status st = h->ensure_vcycle(h->cfg.vcycle_precision);
+  if (st != IPMG_OK) return st;
+#define CK(call, what)                                 \
+  do {                                                 \
+    st = h->cuda((call), what);                        \
+    if (st != IPMG_OK) return st;                      \
+  } while (0)
+  // workspace (grown on demand, kept for later solves)
+  if (h->gcap < max_it) {
+    if (!h->gw && !(h->gw = (double*)h->dalloc(n * 8))) return h->fail(IPMG_ERR_OUT_OF_MEMORY, "GMRES workspace");
+    h->ghcol = (double*)h->dalloc(sizeof(double) * (max_it + 2));
+    h->gy = (double*)h->dalloc(sizeof(double) * (max_it + 1));
+    h->gzptr = (const double**)h->dalloc(sizeof(double*) * (max_it + 1));
+    if (h->ghpin) cudaFreeHost(h->ghpin);
+    h->ghpin = nullptr;
+    if (!h->ghcol || !h->gy || !h->gzptr || cudaMallocHost(&h->ghpin, sizeof(double) * (max_it + 2)) != cudaSuccess)
+      return h->fail(IPMG_ERR_OUT_OF_MEMORY, "GMRES workspace");
+    h->gcap = max_it;
+  }
+  auto vecV = [&](int j) -> double* {
+    while ((int)h->gV.size() <= j) h->gV.push_back((double*)h->dalloc(n * 8));
+    return h->gV[j];
+  };
+  auto vecZ = [&](int j) -> double* {   // operator input: ghosted
+    while ((int)h->gZ.size() <= j) h->gZ.push_back((double*)h->valloc(L, IPMG_FP64));
+    return h->gZ[j];
+  };
+  std::vector<double> hist;
+  // beta0 = ||b||
+  CK(ipmg::dot_partial(0, 0, b, b, n, h->partial, s), "dot");
+  CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
+  h->n_launches += 2;
+  if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
+  CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  const double beta0 = std::sqrt(h->hpin[0]);
+  hist.push_back(beta0);
+  int m = 0;
+  bool conv = beta0 == 0.0;
+  if (conv) {
+    CK(cudaMemsetAsync(x, 0, n * 8, s), "memset x");
+  } else {
+    float* r32 = mixed ? (float*)h->vb[IPMG_FP32][L] : nullptr;
+    const float* z32 = mixed ? (const float*)h->vx1[IPMG_FP32][L] : nullptr;
+    if (!vecV(0)) return h->fail(IPMG_ERR_OUT_OF_MEMORY, "GMRES basis");
+    CK(ipmg::scale_vec(vecV(0), b, n, nullptr, 1.0 / beta0, r32, s), "scale");   // v_0 = b / beta0
+    h->n_launches += 1;
+    // Hessenberg column j, Givens rotations and the rhs g (host, tiny)
+    std::vector<double> H((size_t)(max_it + 1) * max_it, 0.0), cs(max_it), sn(max_it), g(max_it + 1, 0.0);
+    auto Hij = [&](int i, int j) -> double& { return H[(size_t)j * (max_it + 1) + i]; };
+    g[0] = beta0;
+    for (int j = 0; j < max_it; ++j) {
+      double* vj = h->gV[j];
+      double* zj = vecZ(j);
+      double* vn = vecV(j + 1);
+      if (!zj || !vn) return h->fail(IPMG_ERR_OUT_OF_MEMORY, "GMRES basis");
+      // z_j = P^{-1} v_j (right preconditioning; fp32 V-cycle input r32 = (float) v_j)
+      if (mixed) {
+        st = h->vcycle_level(L, IPMG_FP32);
+        if (st != IPMG_OK) return st;
+        CK(ipmg::cast(1, 0, z32, zj, n, s), "cast");
+        h->n_launches += 1;
+      } else {
+        st = h->vcycle(vj, zj, nullptr);
+        if (st != IPMG_OK) return st;
+      }
+      // w = A z_j
+      if ((st = h->halo(L, IPMG_FP64, zj)) != IPMG_OK) return st;
+      st = h->run(KC_VMULT, L, 16.0 * n, 1,
+                  [&] { return h->ks.vmult(h->dim, IPMG_FP64, zj, h->gw, h->geom[L], nullptr, nullptr, nullptr, s); },
+                  "vmult");
+      if (st != IPMG_OK) return st;
+      // modified Gram-Schmidt: h_ij = w.v_i ; w -= h_ij v_i (each step fused with the next dot)
+      CK(ipmg::dot_partial(0, 0, h->gw, h->gV[0], n, h->partial, s), "dot");
+      CK(ipmg::finalize(h->partial, h->ghcol, s), "finalize");
+      h->n_launches += 2;
+      if ((st = h->allsum(h->ghcol)) != IPMG_OK) return st;
+      for (int i = 0; i <= j; ++i) {
+        CK(ipmg::mgs_axpy_dot(h->gw, h->gV[i], i < j ? h->gV[i + 1] : nullptr, n, h->ghcol, i, h->partial, s), "mgs");
+        CK(ipmg::finalize(h->partial, h->ghcol + i + 1, s), "finalize");
+        h->n_launches += 2;
+        if ((st = h->allsum(h->ghcol + i + 1)) != IPMG_OK) return st;
+      }
+      // v_{j+1} = w / ||w|| (and its fp32 copy as the next V-cycle input)
+      CK(ipmg::scale_vec(vn, h->gw, n, h->ghcol + j + 1, 0.0, r32, s), "scale");
+      h->n_launches += 1;
+      CK(cudaMemcpyAsync(h->ghpin, h->ghcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, s), "d2h");
+      CK(cudaStreamSynchronize(s), "sync");
+      for (int i = 0; i <= j; ++i) Hij(i, j) = h->ghpin[i];
+      Hij(j + 1, j) = std::sqrt(h->ghpin[j + 1]);
+      for (int i = 0; i < j; ++i) {   // previous rotations
+        const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
+        Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
+        Hij(i, j) = t;
+      }
+      const double den = std::hypot(Hij(j, j), Hij(j + 1, j));
+      cs[j] = Hij(j, j) / den;
+      sn[j] = Hij(j + 1, j) / den;
+      Hij(j, j) = den;
+      Hij(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      hist.push_back(std::fabs(g[j + 1]));
+      m = j + 1;
+      if (std::fabs(g[j + 1]) <= rtol * beta0) {
+        conv = true;
+        break;
+      }
+    }
+    // y = R^{-1} g (back substitution), x = sum_i y_i z_i
+    std::vector<double> y(m);
+    for (int i = m - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int c = i + 1; c < m; ++c) t -= Hij(i, c) * y[c];
+      y[i] = t / Hij(i, i);
+    }
+    std::vector<const double*> zp(h->gZ.begin(), h->gZ.begin() + m);
+    CK(cudaMemcpyAsync(h->gy, y.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s), "h2d");
+    CK(cudaMemcpyAsync(h->gzptr, zp.data(), sizeof(double*) * m, cudaMemcpyHostToDevice, s), "h2d");
+    CK(ipmg::combine(x, h->gzptr, h->gy, m, n, s), "combine");
+    h->n_launches += 1;
+    CK(cudaStreamSynchronize(s), "sync");   // y, zp are host temporaries
+  }
+#undef CK
+  auto t1 = std::chrono::steady_clock::now();
+  if (info) {
+    info->iterations = m;
+    info->rel_residual = beta0 > 0 ? hist.back() / beta0 : 0.0;
+    info->nu = (m > 0 && info->rel_residual > 0) ? -8.0 * m / std::log10(info->rel_residual) : 0.0;
+    info->seconds = std::chrono::duration<double>(t1 - t0).count();
+    info->history_len = 0;
+    if (info->history && info->history_cap > 0) {
+      const int c = (int)hist.size() < info->history_cap ? (int)hist.size() : info->history_cap;
+      for (int i = 0; i < c; ++i) info->history[i] = hist[i];
+      info->history_len = c;
+    }
+  }
+  if (!conv) return h->fail(IPMG_ERR_NOT_CONVERGED, "ipmg_gmres_solve: max_it reached");
   return IPMG_OK;
 }
 

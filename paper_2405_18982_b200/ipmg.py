@@ -23,7 +23,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "SIZE_MISMATCH", 4: "O
 # every symbol include/ipmg.h declares
 EXPORTS = ["ipmg_config_default", "ipmg_create", "ipmg_destroy", "ipmg_level_info", "ipmg_vmult",
            "ipmg_smooth", "ipmg_smooth_colour", "ipmg_residual_restrict", "ipmg_prolongate_add",
-           "ipmg_coarse_solve", "ipmg_vcycle", "ipmg_cg_solve", "ipmg_rhs", "ipmg_to_cellwise",
+           "ipmg_coarse_solve", "ipmg_vcycle", "ipmg_cg_solve", "ipmg_gmres_solve", "ipmg_rhs", "ipmg_to_cellwise",
            "ipmg_from_cellwise", "ipmg_synchronize", "ipmg_last_error", "ipmg_tables_1d",
            "ipmg_profile", "ipmg_profile_read", "ipmg_launch_count", "ipmg_level_partition", "ipmg_partition",
            "ipmg_nccl_unique_id", "ipmg_comm_create_nccl", "ipmg_comm_create_local", "ipmg_comm_destroy"]
@@ -72,6 +72,7 @@ def load():
         "ipmg_coarse_solve": (i, [vp, i, vp, vp]),
         "ipmg_vcycle": (i, [vp, vp, vp]),
         "ipmg_cg_solve": (i, [vp, vp, vp, d, i, ctypes.POINTER(SolveInfo)]),
+        "ipmg_gmres_solve": (i, [vp, vp, vp, d, i, ctypes.POINTER(SolveInfo)]),
         "ipmg_rhs": (i, [vp, i, i, vp]),
         "ipmg_to_cellwise": (i, [vp, i, i, vp, vp]),
         "ipmg_from_cellwise": (i, [vp, i, i, vp, vp]),
@@ -305,7 +306,14 @@ class Handle:
         self._check(self.lib.ipmg_vcycle(self.h, _ptr(r), _ptr(z)), "vcycle")
 
     def cg_solve(self, b, x, rtol=1e-8, max_it=100):
-        """Returns dict(iterations, nu, rel_residual, seconds, history, converged)."""
+        """PCG (ipmg_cg_solve).  Returns dict(iterations, nu, rel_residual, seconds, history, converged)."""
+        return self._solve(self.lib.ipmg_cg_solve, "cg_solve", b, x, rtol, max_it)
+
+    def gmres_solve(self, b, x, rtol=1e-8, max_it=100):
+        """Right-preconditioned GMRES (ipmg_gmres_solve); same result dict as cg_solve."""
+        return self._solve(self.lib.ipmg_gmres_solve, "gmres_solve", b, x, rtol, max_it)
+
+    def _solve(self, fn, what, b, x, rtol, max_it):
         L = self.n_levels - 1
         self._vec(b, L, FP64), self._vec(x, L, FP64)
         cap = max_it + 2
@@ -313,9 +321,9 @@ class Handle:
         info = SolveInfo()
         info.history = hist
         info.history_cap = cap
-        st = self.lib.ipmg_cg_solve(self.h, _ptr(b), _ptr(x), rtol, max_it, ctypes.byref(info))
+        st = fn(self.h, _ptr(b), _ptr(x), rtol, max_it, ctypes.byref(info))
         if st not in (IPMG_OK, IPMG_ERR_NOT_CONVERGED):
-            self._check(st, "cg_solve")
+            self._check(st, what)
         return dict(iterations=info.iterations, nu=info.nu, rel_residual=info.rel_residual,
                     seconds=info.seconds, history=list(hist[:info.history_len]),
                     converged=(st == IPMG_OK))

@@ -267,3 +267,21 @@ def test_too_many_ranks_rejected():
     finally:
         for c in comms:
             c.close()
+
+
+def test_gmres_matches_serial():
+    _need_gpu()
+    t = Team(3, 3, 4, 2, None)
+    try:
+        L = t.nl - 1
+        b = torch.empty(t.serial.ndofs(L), dtype=torch.float64, device="cuda")
+        t.serial.rhs(L, b)
+        x = torch.empty_like(b)
+        res = t.serial.gmres_solve(b, x)
+        bs = t.split(L, b)
+        xs = [torch.empty_like(v) for v in bs]
+        out = t.run(lambda r, h: h.gmres_solve(bs[r], xs[r]))
+        assert all(o["iterations"] == res["iterations"] for o in out)
+        assert float(torch.linalg.norm(t.join(L, xs) - x) / torch.linalg.norm(x)) <= 1e-10
+    finally:
+        t.close()

@@ -243,3 +243,39 @@ def test_cg_solve(case, vprec):
     # true residual of the GPU solution, evaluated by the oracle
     xg = to_cw(h, L, x)
     assert np.linalg.norm(b - ops[L] @ xg) <= 1.5e-8 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("case", [(2, 2, 3, None), (2, 5, 4, None), (3, 2, 3, None), (3, 3, 3, None)],
+                         ids=["C1_d2k2", "d2k5", "d3k2", "d3k3"])
+@pytest.mark.parametrize("vprec", [0, 1], ids=["fp64", "mixed"])
+def test_gmres_solve(case, vprec):
+    """NEXT-2: right-preconditioned GMRES (MGS, no restart) against the oracle's
+    GMRES (oracle/krylov.py) on f == 1: same iteration count (+-1), the
+    least-squares residual history, the solution, and nu."""
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle(dim, k, nl, coarse, vprec)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    V = multigrid.VCycle(dim, k, nl, n0=coarse, operators=ops,
+                         dtype=np.float64 if vprec == 0 else np.float32)
+    L = nl - 1
+    b = assemble.rhs(levels[L], k)
+    xo, hist, conv = krylov.gmres(ops[L], b, V, rtol=1e-8)
+    bl = torch.empty(len(b), dtype=torch.float64, device="cuda")
+    h.rhs(L, bl)
+    x = torch.empty_like(bl)
+    res = h.gmres_solve(bl, x, rtol=1e-8, max_it=60)
+    assert res["converged"] and conv
+    assert abs(res["iterations"] - (len(hist) - 1)) <= 1
+    m = min(len(hist), len(res["history"]))
+    # fp32 V-cycle rounding (~1e-7 relative) enters the Krylov basis in mixed mode
+    htol, hatol = (1e-9, 1e-12) if vprec == 0 else (5e-2, 1e-7)
+    assert np.allclose(res["history"][:m], hist[:m], rtol=htol, atol=hatol * hist[0])
+    assert abs(res["nu"] - krylov.nu(hist)) <= (1e-6 if vprec == 0 else 0.3)
+    xg = to_cw(h, L, x)
+    if res["iterations"] == len(hist) - 1:
+        assert rel(xg, xo) <= (1e-12 if vprec == 0 else 1e-6)
+    assert np.linalg.norm(b - ops[L] @ xg) <= 1.5e-8 * np.linalg.norm(b)
+    # a second solve reuses the library-owned Krylov basis
+    res2 = h.gmres_solve(bl, x, rtol=1e-8, max_it=60)
+    assert res2["iterations"] == res["iterations"]
