@@ -52,8 +52,11 @@ typedef enum {
 
 typedef enum { IPMG_FP64 = 0, IPMG_FP32 = 1 } ipmg_precision;
 
-/* Local solver of the vertex-patch smoother ("full" kernel). */
-typedef enum { IPMG_KERNEL_FULL = 0 } ipmg_kernel;
+/* Local solver of the vertex-patch smoother: FULL = PAPER.md:199 (V_j = all patch
+ * dofs, exact residual from the face neighbours); DIRICHLET = PAPER.md:212-225
+ * (V_j without the outer nodes at mesh-interior patch faces, residual from the
+ * patch cells only -- inconsistent, use GMRES; reading A20). */
+typedef enum { IPMG_KERNEL_FULL = 0, IPMG_KERNEL_DIRICHLET = 1 } ipmg_kernel;
 
 /* Multiplicative = Algorithm 1; additive = BASELINE.json
  * configs[4] (damped, omega default 1/2^d, reading A17). */
@@ -237,7 +240,9 @@ const char *ipmg_last_error(const ipmg_handle *h);
  * 2 stiffness (k+1)^2, 3+v patch matrix L^P_v (2k+2)^2 for variant v in 0..3
  * (bit0: low face on boundary, bit1: high face on boundary), 7+v patch
  * eigenvectors S_v (row-major, column m = mode m), 11+v eigenvalues (2k+2),
- * 15 prolongation (2k+2)x(k+1).  Writes at most cap doubles to out (host);
+ * 15 prolongation (2k+2)x(k+1); Dirichlet kernel: 16+v residual patch matrix
+ * (no mesh-interior outer faces), 20+v padded local eigenvectors, 24+v their
+ * eigenvalues, 28+v mode activity (1/0).  Writes at most cap doubles to out (host);
  * *len = number of entries.  Errors: UNSUPPORTED (k), INVALID_ARG. */
 ipmg_status ipmg_tables_1d(int k, double penalty_scale, int what, double *out, int cap, int *len);
 

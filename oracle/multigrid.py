@@ -19,7 +19,7 @@ from .smoother import PatchSmoother
 class VCycle:
     def __init__(self, dim, k, n_levels, n0=None, h0=0.5, dtype=np.float64,
                  smoother="multiplicative", omega=None, post_reverse=True,
-                 penalty_scale=1.0, operators=None):
+                 penalty_scale=1.0, operators=None, kernel="full"):
         self.dim, self.k, self.n_levels = dim, k, n_levels
         self.dtype = np.dtype(dtype)
         self.levels = mesh.hierarchy(dim, n_levels, n0, h0)
@@ -29,7 +29,8 @@ class VCycle:
         self.A = [A.astype(self.dtype) for A in operators]
         self.P = [None] + [transfer.prolongation(self.levels[l - 1], self.levels[l], k).astype(self.dtype)
                            for l in range(1, n_levels)]
-        self.S = [None] + [PatchSmoother(self.levels[l], k, operators[l], self.dtype)
+        self.S = [None] + [PatchSmoother(self.levels[l], k, operators[l], self.dtype, kernel=kernel,
+                                         penalty_scale=penalty_scale)
                            for l in range(1, n_levels)]
         self.coarse_lu = sla.lu_factor(self.A[0].toarray())
         self.kind, self.omega, self.post_reverse = smoother, omega, post_reverse

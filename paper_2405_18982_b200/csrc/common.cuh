@@ -69,6 +69,7 @@ struct TabData {
                                     // 0 low/u, 1 low/u', 2 high/u, 3 high/u'  (see face_* kernels)
   alignas(16) T CH[4][4][RP];       // the same in eigen-space: CH[v][kind][m] = sum_i S[v][i][m] CF[kind][i]
   alignas(16) T lam[4][RP];         // eigenvalues
+  alignas(16) T act[4][RP];         // 1 / 0: mode active (Dirichlet tables; all 1 for the full kernel)
   alignas(16) T d0[RC];             // phi_j'(0)
   alignas(16) T d1[RC];             // phi_j'(1)
   alignas(16) T P[NP][RC];          // prolongation (patch-lex fine node, coarse node)

@@ -113,7 +113,14 @@ void add_face(std::vector<double>& A, int n, const std::vector<double>& jv,
 // 1D SIPG matrix on `ncell` unit cells; `low_bnd` / `high_bnd`: outer faces
 // are domain-boundary faces (full Nitsche terms) rather than
 // interior faces whose neighbour lies outside (self-terms with weight 1/2).
+// outer faces: 0 mesh-interior (the chain's side of the face, weight 1/2),
+// 1 domain boundary (Nitsche, weight 1), 2 omitted
+std::vector<double> sipg_chain_modes(const FE1D& fe, int ncell, int low_mode, int high_mode);
 std::vector<double> sipg_chain(const FE1D& fe, int ncell, bool low_bnd, bool high_bnd) {
+  return sipg_chain_modes(fe, ncell, low_bnd ? 1 : 0, high_bnd ? 1 : 0);
+}
+std::vector<double> sipg_chain_modes(const FE1D& fe, int ncell, int low_mode, int high_mode) {
+  const bool low_bnd = low_mode == 1, high_bnd = high_mode == 1;
   const int nc = fe.nc, n = ncell * nc;
   std::vector<double> A(n * n, 0.0);
   for (int c = 0; c < ncell; ++c)
@@ -133,7 +140,7 @@ std::vector<double> sipg_chain(const FE1D& fe, int ncell, bool low_bnd, bool hig
     add_face(A, n, jv, gv, fe.gamma);
   }
   // low outer face: the chain is the "B" (right) side; J = -vB, G = w * gB
-  {
+  if (low_mode != 2) {
     std::fill(jv.begin(), jv.end(), 0.0);
     std::fill(gv.begin(), gv.end(), 0.0);
     const double wt = low_bnd ? 1.0 : 0.5;
@@ -142,7 +149,7 @@ std::vector<double> sipg_chain(const FE1D& fe, int ncell, bool low_bnd, bool hig
     add_face(A, n, jv, gv, fe.gamma);
   }
   // high outer face: the chain is the "A" (left) side; J = vA, G = w * gA
-  {
+  if (high_mode != 2) {
     std::fill(jv.begin(), jv.end(), 0.0);
     std::fill(gv.begin(), gv.end(), 0.0);
     const double wt = high_bnd ? 1.0 : 0.5;
@@ -317,6 +324,68 @@ FE1D build_fe1d(int k, double penalty_scale) {
       fe.S[0] = S2;
       fe.lam[0] = l2;
       fe.even_odd = true;
+    }
+  }
+  // ---- Dirichlet kernel tables (reading A20)
+  fe.even_odd_dir = false;
+  for (int var = 0; var < 4; ++var) {
+    const bool lo_b = var & 1, hi_b = var & 2;
+    fe.LPR[var] = sipg_chain_modes(fe, 2, lo_b ? 1 : 2, hi_b ? 1 : 2);
+    std::vector<int> keep;
+    for (int i = 0; i < np; ++i)
+      if (!((i == 0 && !lo_b) || (i == np - 1 && !hi_b))) keep.push_back(i);
+    const int nk = (int)keep.size();
+    std::vector<double> Lk(nk * nk), Mk(nk * nk), Sk, lk;
+    for (int a = 0; a < nk; ++a)
+      for (int b = 0; b < nk; ++b) {
+        Lk[a * nk + b] = fe.LP[var][keep[a] * np + keep[b]];   // = LPR on kept nodes (outer terms vanish there)
+        Mk[a * nk + b] = fe.MP[keep[a] * np + keep[b]];
+      }
+    gen_eig(nk, Lk, Mk, Sk, lk);
+    std::vector<double>& S = fe.SD[var];
+    S.assign(np * np, 0.0);
+    fe.lamD[var].assign(np, 1.0);
+    fe.actD[var].assign(np, 0.0);
+    if (var == 0) {
+      // reflection-symmetric: split the nk = np-2 modes into even / odd, then
+      // prepend the inactive boundary pair to each half
+      std::vector<int> ev, od;
+      for (int m = 0; m < nk; ++m) {
+        double se = 0.0, so = 0.0;
+        for (int a = 0; a < nk; ++a) {
+          se += std::fabs(Sk[a * nk + m] - Sk[(nk - 1 - a) * nk + m]);
+          so += std::fabs(Sk[a * nk + m] + Sk[(nk - 1 - a) * nk + m]);
+        }
+        (se < so ? ev : od).push_back(m);
+      }
+      if ((int)ev.size() != nk / 2 || (int)od.size() != nk / 2) continue;
+      const double r2 = std::sqrt(0.5);
+      for (int h = 0; h < 2; ++h) {
+        const int base = h * (np / 2);
+        const double sg = h == 0 ? 1.0 : -1.0;
+        S[0 * np + base] = r2;
+        S[(np - 1) * np + base] = sg * r2;
+        for (int q = 0; q < nk / 2; ++q) {
+          const int m = h == 0 ? ev[q] : od[q], col = base + 1 + q;
+          fe.lamD[var][col] = lk[m];
+          fe.actD[var][col] = 1.0;
+          for (int a = 0; a < nk / 2; ++a) {   // exact symmetrisation
+            const double v = 0.5 * (Sk[a * nk + m] + sg * Sk[(nk - 1 - a) * nk + m]);
+            S[keep[a] * np + col] = v;
+            S[keep[nk - 1 - a] * np + col] = sg * v;
+          }
+        }
+      }
+      fe.even_odd_dir = true;
+    } else {
+      int col = 0;
+      for (int m = 0; m < nk; ++m, ++col) {
+        fe.lamD[var][col] = lk[m];
+        fe.actD[var][col] = 1.0;
+        for (int a = 0; a < nk; ++a) S[keep[a] * np + col] = Sk[a * nk + m];
+      }
+      for (int i = 0; i < np; ++i)   // inactive unit modes on the dropped nodes
+        if (std::find(keep.begin(), keep.end(), i) == keep.end()) S[i * np + col++] = 1.0;
     }
   }
   fe.P.assign(np * nc, 0.0);

@@ -31,6 +31,14 @@ struct FE1D {
   std::vector<double> lam[4];      // eigenvalues (variant 0: even modes then odd modes, each ascending)
   bool even_odd = false;           // variant-0 modes ordered [even | odd] (always true in practice)
   std::vector<double> P;           // prolongation, P[i*nc+j] = phi_j((xi_{i%nc} + i/nc)/2)  (np*nc)
+  // Dirichlet kernel (reading A20), variant v as above:
+  //  LPR[v]  patch matrix WITHOUT the mesh-interior outer faces (the residual operator)
+  //  SD[v]   eigenvectors of the local problem on the kept nodes (outer nodes at
+  //          mesh-interior faces dropped), padded to np x np; excluded nodes get
+  //          inactive modes (actD = 0).  Variant 0: [even | odd], the boundary pair
+  //          (e_0 +- e_{np-1})/sqrt2 is the first mode of each half.
+  std::vector<double> LPR[4], SD[4], lamD[4], actD[4];
+  bool even_odd_dir = false;
 };
 
 // Build all unit tables for degree k (1..7); penalty_scale multiplies gamma.

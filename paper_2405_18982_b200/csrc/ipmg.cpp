@@ -25,6 +25,13 @@ ipmg::KernelSet ipmg_kernel_set_k4();
 ipmg::KernelSet ipmg_kernel_set_k5();
 ipmg::KernelSet ipmg_kernel_set_k6();
 ipmg::KernelSet ipmg_kernel_set_k7();
+ipmg::KernelSet ipmg_kernel_set_dir_k1();
+ipmg::KernelSet ipmg_kernel_set_dir_k2();
+ipmg::KernelSet ipmg_kernel_set_dir_k3();
+ipmg::KernelSet ipmg_kernel_set_dir_k4();
+ipmg::KernelSet ipmg_kernel_set_dir_k5();
+ipmg::KernelSet ipmg_kernel_set_dir_k6();
+ipmg::KernelSet ipmg_kernel_set_dir_k7();
 
 namespace {
 
@@ -52,6 +59,17 @@ ipmg::KernelSet kernel_set(int k) {
     default: return ipmg_kernel_set_k7();
   }
 }
+ipmg::KernelSet kernel_set_dir(int k) {
+  switch (k) {
+    case 1: return ipmg_kernel_set_dir_k1();
+    case 2: return ipmg_kernel_set_dir_k2();
+    case 3: return ipmg_kernel_set_dir_k3();
+    case 4: return ipmg_kernel_set_dir_k4();
+    case 5: return ipmg_kernel_set_dir_k5();
+    case 6: return ipmg_kernel_set_dir_k6();
+    default: return ipmg_kernel_set_dir_k7();
+  }
+}
 
 }  // namespace
 
@@ -63,6 +81,7 @@ struct ipmg_handle {
   int dim = 3, k = 1, nc = 2, cell = 8, nlev = 1;
   cudaStream_t stream = nullptr;
   ipmg::KernelSet ks{};
+  ipmg::KernelSet ksd{};              // Dirichlet-kernel smoother (cfg.kernel == IPMG_KERNEL_DIRICHLET)
   ipmg::FE1D fe;
   std::vector<ipmg::LevelGeom> geom;
   std::vector<long long> ndofs;
@@ -212,7 +231,11 @@ struct ipmg_handle {
   // ------------------------------------------------------------ building blocks
   ipmg_status smooth_colour(int level, int prec, const void* xi, const void* b, void* xo, int colour) {
     return run(KC_SMOOTH, level, smooth_bytes(level, prec, colour, xi != nullptr), 1,
-               [&] { return ks.smooth(dim, prec, xi, b, xo, geom[level], colour, stream); }, "smooth_colour");
+               [&] {
+                 return (cfg.kernel == IPMG_KERNEL_DIRICHLET ? ksd : ks).smooth(dim, prec, xi, b, xo, geom[level], colour,
+                                                                                stream);
+               },
+               "smooth_colour");
   }
   // multiplicative step: passes ping-pong between x and other; 2^d passes -> ends in x
   ipmg_status smooth_mult(int level, int prec, void* x, void* other, const void* b, bool reverse, bool x_is_zero) {
@@ -388,7 +411,7 @@ const char* ipmg_last_error(const ipmg_handle* h) { return h ? h->err.c_str() : 
 
 ipmg_status ipmg_tables_1d(int k, double penalty_scale, int what, double* out, int cap, int* len) {
   if (k < 1 || k > 7) return IPMG_ERR_UNSUPPORTED;
-  if (!out || !len || what < 0 || what > 15) return IPMG_ERR_INVALID_ARG;
+  if (!out || !len || what < 0 || what > 31) return IPMG_ERR_INVALID_ARG;
   ipmg::FE1D fe = ipmg::build_fe1d(k, penalty_scale);
   const std::vector<double>* src = nullptr;
   if (what == 0) src = &fe.nodes;
@@ -397,7 +420,11 @@ ipmg_status ipmg_tables_1d(int k, double penalty_scale, int what, double* out, i
   else if (what <= 6) src = &fe.LP[what - 3];
   else if (what <= 10) src = &fe.S[what - 7];
   else if (what <= 14) src = &fe.lam[what - 11];
-  else src = &fe.P;
+  else if (what == 15) src = &fe.P;
+  else if (what <= 19) src = &fe.LPR[what - 16];
+  else if (what <= 23) src = &fe.SD[what - 20];
+  else if (what <= 27) src = &fe.lamD[what - 24];
+  else src = &fe.actD[what - 28];
   *len = (int)src->size();
   if ((int)src->size() > cap) return IPMG_ERR_SIZE_MISMATCH;
   std::memcpy(out, src->data(), src->size() * sizeof(double));
@@ -418,7 +445,14 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
       g_create_error = "coarse_cells must be 1 or 2 per direction";
       return IPMG_ERR_INVALID_ARG;
     }
-  if (cfg->kernel != IPMG_KERNEL_FULL) { g_create_error = "only the full kernel is implemented"; return IPMG_ERR_UNSUPPORTED; }
+  if (cfg->kernel != IPMG_KERNEL_FULL && cfg->kernel != IPMG_KERNEL_DIRICHLET) {
+    g_create_error = "kernel must be IPMG_KERNEL_FULL or IPMG_KERNEL_DIRICHLET";
+    return IPMG_ERR_UNSUPPORTED;
+  }
+  if (cfg->kernel == IPMG_KERNEL_DIRICHLET && cfg->smoother != IPMG_MULTIPLICATIVE) {
+    g_create_error = "the Dirichlet kernel is a multiplicative smoother (Algorithm 1)";
+    return IPMG_ERR_UNSUPPORTED;
+  }
   if (cfg->smoother != IPMG_MULTIPLICATIVE && cfg->smoother != IPMG_ADDITIVE) {
     g_create_error = "unknown smoother";
     return IPMG_ERR_INVALID_ARG;
@@ -456,6 +490,15 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   h->ks = kernel_set(h->k);
   {
     ipmg_status st = h->cuda(h->ks.upload(h->fe), "table upload");
+    if (st != IPMG_OK) return bail(st);
+  }
+  if (cfg->kernel == IPMG_KERNEL_DIRICHLET) {
+    if (!h->fe.even_odd_dir) {
+      h->err = "Dirichlet interior eigenvectors are not even/odd";
+      return bail(IPMG_ERR_UNSUPPORTED);
+    }
+    h->ksd = kernel_set_dir(h->k);
+    ipmg_status st = h->cuda(h->ksd.upload(h->fe), "Dirichlet table upload");
     if (st != IPMG_OK) return bail(st);
   }
   // ---- hierarchy, slab partition of every level

@@ -1,0 +1,4 @@
+// Dirichlet-kernel smoother for degree k=7 (see patch_kernels.cuh, IPMG_DIRICHLET).
+#define IPMG_K 7
+#define IPMG_DIRICHLET 1
+#include "patch_kernels.cuh"

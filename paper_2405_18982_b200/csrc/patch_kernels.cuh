@@ -41,12 +41,23 @@
 #define IPMG_CAT(a, b) IPMG_CAT2(a, b)
 // every degree lives in its own namespace: the per-TU __constant__ tables and
 // the kernel template instantiations must not collide at link time
+// The Dirichlet-kernel translation units (kernels_dir_k<K>.cu, IPMG_DIRICHLET = 1)
+// fill the same table layout with the Dirichlet tables (LP <- LPR, S <- SD,
+// lam <- lamD, act <- actD) in their own constant bank (64 KB per module).
+#ifndef IPMG_DIRICHLET
+#define IPMG_DIRICHLET 0
+#endif
+#if IPMG_DIRICHLET
+#define IPMG_KK IPMG_CAT(kdir, IPMG_K)
+#else
 #define IPMG_KK IPMG_CAT(kdeg, IPMG_K)
+#endif
 
 namespace ipmg {
 namespace IPMG_KK {
 
 constexpr int K = IPMG_K;
+constexpr bool kDir = IPMG_DIRICHLET != 0;
 constexpr int NC = K + 1;
 constexpr int NP = 2 * NC;
 
@@ -1187,24 +1198,31 @@ __device__ __forceinline__ void bwd_line(const T (&v)[R][NP], T (&w)[R][NP], int
 
 // S^T, scale by 1/(lsum + lambda_m), S on R lines of the last direction (variant V)
 template <int V, int R, typename T>
-__device__ __forceinline__ void fd_last(T (&v)[R][NP], T (&w)[R][NP], const T (&lsum)[R]) {
+__device__ __forceinline__ void fd_last(T (&v)[R][NP], T (&w)[R][NP], const T (&lsum)[R], const T (&lact)[R]) {
   static_assert(V == 0, "fast path is the interior variant");
   const TabData<K, T>& tb = tab<T>();
   eigT_eo<R>(v, w);
 #pragma unroll
   for (int m = 0; m < NP; ++m)
 #pragma unroll
-    for (int r = 0; r < R; ++r) w[r][m] *= rcp_(lsum[r] + tb.lam[0][m]);
+    for (int r = 0; r < R; ++r) {
+      if (kDir) w[r][m] *= (lact[r] * tb.act[0][m]) * rcp_(lsum[r] + tb.lam[0][m]);   // exact 0 when inactive
+      else w[r][m] *= rcp_(lsum[r] + tb.lam[0][m]);
+    }
   eig_eo<R>(w, v);
 }
 template <int R, typename T>
-__device__ __forceinline__ void fd_last_rt(T (&v)[R][NP], T (&w)[R][NP], const T (&lsum)[R], int var) {
+__device__ __forceinline__ void fd_last_rt(T (&v)[R][NP], T (&w)[R][NP], const T (&lsum)[R], const T (&lact)[R],
+                                           int var) {
   const TabData<K, T>& tb = tab<T>();
   mv<NP, NP, EigTRT<T>, R>(v, w, EigTRT<T>{var});
 #pragma unroll
   for (int m = 0; m < NP; ++m)
 #pragma unroll
-    for (int r = 0; r < R; ++r) w[r][m] *= rcp_(lsum[r] + tb.lam[var][m]);
+    for (int r = 0; r < R; ++r) {
+      if (kDir) w[r][m] *= (lact[r] * tb.act[var][m]) * rcp_(lsum[r] + tb.lam[var][m]);
+      else w[r][m] *= rcp_(lsum[r] + tb.lam[var][m]);
+    }
   mv<NP, NP, EigRT<T>, R>(w, v, EigRT<T>{var});
 }
 
@@ -1242,17 +1260,22 @@ __device__ void fd_post(T* X, const T* F, const PInfo<D>* pis, int npc, Out&& ou
   const TabData<K, T>& tb = tab<T>();
   for_groups<D, T>(LAST, npc, [&](int p, int g, int base, int gap, int stride) {
     const PInfo<D>& pi = pis[p];
-    T lsum[R];
+    T lsum[R], lact[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int l = g + r * C::G;           // line id: (m0) in 2D, (m0 + NP m1) in 3D
       lsum[r] = tb.lam[pi.var[0]][l % NP];
       if (D == 3) lsum[r] += tb.lam[pi.var[1]][l / NP];
+      lact[r] = T(1);
+      if (kDir) {   // Dirichlet: a line through an inactive mode of another direction is zero
+        lact[r] = tb.act[pi.var[0]][l % NP];
+        if (D == 3) lact[r] *= tb.act[pi.var[1]][l / NP];
+      }
     }
     T v[R][NP], w[R][NP];
     load_lines<NP, R>(X + base, gap, stride, v);
     if (FACES) face_inject<D, -1, R>(v, F, p, LAST, g);
-    IPMG_VAR_SPLIT(pi.var[LAST], (fd_last<0, R>(v, w, lsum)), (fd_last_rt<R>(v, w, lsum, v_)));
+    IPMG_VAR_SPLIT(pi.var[LAST], (fd_last<0, R>(v, w, lsum, lact)), (fd_last_rt<R>(v, w, lsum, lact, v_)));
     store_lines<NP, R>(X + base, gap, stride, v);
   });
   __syncthreads();
@@ -1697,6 +1720,98 @@ cudaError_t launch_prolong(const void* ec, void* xf, const LevelGeom& gf, const 
   return cudaGetLastError();
 }
 
+#if IPMG_DIRICHLET
+// ---------------------------------------------------------------- Dirichlet kernel (NEXT-1)
+// hinv * b gathered along the lines of the LAST direction (the vol_last layout)
+template <int D, int R, typename T>
+__device__ __forceinline__ void gather_last_lines(const T* __restrict__ src, const PInfo<D>& pi, int g, T scale,
+                                                  T (&v)[R][NP]) {
+  using C = Cfg<D, T>;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int l = g + r * C::G;
+    const int i0 = l % NP, i1 = (D == 3) ? l / NP : 0;
+    const int qb = (i0 / NC) + (D == 3 ? 2 * (i1 / NC) : 0);
+    const int ob = (i0 % NC) + (D == 3 ? NC * (i1 % NC) : 0);
+    constexpr int QS = (D == 2) ? 2 : 4, SS = (D == 2) ? NC : NC * NC;
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+      v[r][j] = pi.valid ? scale * __ldg(src + (j < NC ? pi.coff[qb] : pi.coff[qb + QS]) + ob + (j % NC) * SS) : T(0);
+  }
+}
+
+// One colour of Algorithm 1 with the Dirichlet kernel (reading
+// A20): per patch j, r = hinv b - A~ x_patch with A~ the patch operator without
+// its mesh-interior outer faces (only the patch's own cells are read -- the
+// domain of dependence of the continuous method), delta = A_jj^{-1} r on V_j
+// (outer nodes at mesh-interior faces dropped: inactive modes of the padded
+// eigenbasis), x_out = x_in + delta on the patch cells.  The extra CTA column
+// copies the cells the colour does not cover.
+template <int D, typename T>
+__global__ void __launch_bounds__(Cfg<D, T>::NT)
+    smooth_dir_kernel(const T* __restrict__ x_in, const T* __restrict__ b, T* __restrict__ x_out, LevelGeom g,
+                      int colour, int nbx) {
+  using C = Cfg<D, T>;
+  constexpr int R = C::R;
+  if ((int)blockIdx.x >= nbx) {
+    const long long q = blockIdx.y + (long long)gridDim.y * blockIdx.z;
+    copy_uncovered_part<D, T>(x_in, x_out, g, colour, q * blockDim.x + threadIdx.x,
+                              (long long)gridDim.y * gridDim.z * blockDim.x);
+    return;
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* X = reinterpret_cast<T*>(smem_raw);
+  T* T1 = X + C::PPC * C::TSZ;
+  __shared__ PInfo<D> pis[C::PPC];
+  setup_patches<D, T>(pis, g, colour);
+  T xr[R][NP];
+  my_rows<D>(x_in, pis, C::PPC, T(1), xr);   // zeros when x_in == nullptr
+  vol_pre<D, false>(xr, X, T1, (const T*)nullptr, pis, C::PPC);
+  const T hinv = T(g.hinv);
+  vol_last<D, false>(X, T1, (const T*)nullptr, pis, C::PPC,
+                     [&](int p, int gg, int base, int gap, int stride, const T (&yy)[R][NP]) {
+                       T rr[R][NP];
+                       gather_last_lines<D, R>(b, pis[p], gg, hinv, rr);
+#pragma unroll
+                       for (int r = 0; r < R; ++r)
+#pragma unroll
+                         for (int j = 0; j < NP; ++j) rr[r][j] -= yy[r][j];
+                       store_lines<NP, R>(X + base, gap, stride, rr);
+                     });
+  __syncthreads();
+  T r0[R][NP];
+  for_groups<D, T>(0, C::PPC, [&](int, int, int base, int gap, int stride) { load_lines<NP, R>(X + base, gap, stride, r0); });
+  fd_pre<D, false>(r0, X, (const T*)nullptr, pis, C::PPC);
+  if (x_in != nullptr)
+    fd_post<D, false>(X, (const T*)nullptr, pis, C::PPC, [&](int p, int gg, const T (&w)[R][NP]) {
+      store_rows<D, 2, R>(x_out, x_in, pis[p], gg, T(-1), w);   // x_in + delta
+    });
+  else
+    fd_post<D, false>(X, (const T*)nullptr, pis, C::PPC, [&](int p, int gg, const T (&w)[R][NP]) {
+      store_rows<D, 0, R>(x_out, (const T*)nullptr, pis[p], gg, T(1), w);
+    });
+}
+
+template <int D, typename T>
+cudaError_t launch_smooth_dir(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
+  using C = Cfg<D, T>;
+  const dim3 grid = patch_grid<D, T>(g, colour);
+  const size_t sm = smem_bytes<D, T>(2, false);
+  cudaError_t e = set_smem(smooth_dir_kernel<D, T>, sm);
+  if (e != cudaSuccess) return e;
+  if (grid.x * grid.y * grid.z > 0) {
+    const dim3 g2(grid.x + (colour != 0 ? 1 : 0), grid.y, grid.z);
+    smooth_dir_kernel<D, T><<<g2, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour, (int)grid.x);
+    return cudaGetLastError();
+  }
+  if (colour != 0) {
+    copy_uncovered_kernel<D, T><<<4 * 148, 256, 0, s>>>((const T*)xi, (T*)xo, g, colour);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+#endif
+
 // runtime (dim, prec) dispatch
 #define IPMG_DISPATCH(dim, prec, FN, ...)                                               \
   ((dim) == 2 ? ((prec) == 0 ? FN<2, double>(__VA_ARGS__) : FN<2, float>(__VA_ARGS__)) \
@@ -1709,13 +1824,20 @@ void fill_tab(TabData<K, T>& t, const FE1D& fe) {
   for (int i = 0; i < NC; ++i)
     for (int j = 0; j < NC; ++j) t.M[i][j] = (T)fe.M[i * NC + j];
   for (int v = 0; v < 4; ++v) {
+    // Dirichlet TUs: residual operator without the mesh-interior outer faces and
+    // the padded local eigenbasis with its activity flags (fe1d.cpp, reading A20)
+    const std::vector<double>& LPv = kDir ? fe.LPR[v] : fe.LP[v];
+    const std::vector<double>& Sv = kDir ? fe.SD[v] : fe.S[v];
     for (int i = 0; i < NP; ++i)
       for (int j = 0; j < NP; ++j) {
-        t.LP[v][i][j] = (T)fe.LP[v][i * NP + j];
-        t.S[v][i][j] = (T)fe.S[v][i * NP + j];
-        t.ST[v][j][i] = (T)fe.S[v][i * NP + j];
+        t.LP[v][i][j] = (T)LPv[i * NP + j];
+        t.S[v][i][j] = (T)Sv[i * NP + j];
+        t.ST[v][j][i] = (T)Sv[i * NP + j];
       }
-    for (int i = 0; i < NP; ++i) t.lam[v][i] = (T)fe.lam[v][i];
+    for (int i = 0; i < NP; ++i) {
+      t.lam[v][i] = (T)(kDir ? fe.lamD[v][i] : fe.lam[v][i]);
+      t.act[v][i] = (T)(kDir ? fe.actD[v][i] : 1.0);
+    }
   }
   for (int v = 0; v < 4; ++v)
     for (int i = 0; i < NP; ++i)
@@ -1766,6 +1888,12 @@ inline cudaError_t upload(const FE1D& fe) {
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(c_tab32, &t32, sizeof(t32));
 }
+#if IPMG_DIRICHLET
+inline cudaError_t smooth_dir(int dim, int prec, const void* xi, const void* b, void* xo, const LevelGeom& g, int c,
+                              cudaStream_t s) {
+  return IPMG_DISPATCH(dim, prec, launch_smooth_dir, xi, b, xo, g, c, s);
+}
+#else
 inline cudaError_t vmult(int dim, int prec, const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp,
                          long long* nparts, cudaStream_t s) {
   return IPMG_DISPATCH(dim, prec, launch_vmult, x, y, g, bm, dotp, nparts, s);
@@ -1786,10 +1914,21 @@ inline cudaError_t prolong(int dim, int prec, const void* ec, void* xf, const Le
                            cudaStream_t s) {
   return IPMG_DISPATCH(dim, prec, launch_prolong, ec, xf, gf, gc, s);
 }
+#endif
 
 }  // namespace IPMG_KK
 }  // namespace ipmg
 
+#if IPMG_DIRICHLET
+// Dirichlet-kernel set: only the table upload and the smoother colour pass
+extern "C++" ipmg::KernelSet IPMG_CAT(ipmg_kernel_set_dir_k, IPMG_K)() {
+  ipmg::KernelSet ks{};
+  ks.k = IPMG_K;
+  ks.upload = ipmg::IPMG_KK::upload;
+  ks.smooth = ipmg::IPMG_KK::smooth_dir;
+  return ks;
+}
+#else
 extern "C++" ipmg::KernelSet IPMG_CAT(ipmg_kernel_set_k, IPMG_K)() {
   ipmg::KernelSet ks;
   ks.k = IPMG_K;
@@ -1801,3 +1940,4 @@ extern "C++" ipmg::KernelSet IPMG_CAT(ipmg_kernel_set_k, IPMG_K)() {
   ks.prolong = ipmg::IPMG_KK::prolong;
   return ks;
 }
+#endif

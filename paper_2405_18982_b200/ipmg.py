@@ -17,6 +17,7 @@ IPMG_OK = 0
 IPMG_ERR_NOT_CONVERGED = 7
 FP64, FP32 = 0, 1
 MULTIPLICATIVE, ADDITIVE = 0, 1
+KERNEL_FULL, KERNEL_DIRICHLET = 0, 1
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "SIZE_MISMATCH", 4: "OUT_OF_MEMORY",
           5: "CUDA", 6: "NCCL", 7: "NOT_CONVERGED"}
 
@@ -190,7 +191,7 @@ class Handle:
 
     def __init__(self, dim, degree, n_levels, coarse_cells=None, h0=0.5, smoother=MULTIPLICATIVE,
                  additive_omega=0.0, post_smooth_reverse=1, vcycle_precision=FP32, penalty_scale=1.0,
-                 device=0, stream=None, comm=None):
+                 device=0, stream=None, comm=None, kernel=KERNEL_FULL):
         import torch
         self.lib = load()
         cfg = Config()
@@ -202,6 +203,7 @@ class Handle:
         cfg.smoother, cfg.additive_omega = smoother, additive_omega
         cfg.post_smooth_reverse, cfg.vcycle_precision = post_smooth_reverse, vcycle_precision
         cfg.penalty_scale, cfg.device = penalty_scale, device
+        cfg.kernel = kernel
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream

@@ -84,3 +84,38 @@ def test_penalty_scale_changes_tables():
     a = ipmg.tables_1d(2, 6, 1.0)
     b = ipmg.tables_1d(2, 6, 2.0)
     assert np.abs(a - b).max() > 1.0
+
+
+@pytest.mark.parametrize("k", [1, 3, 5, 7])
+def test_dirichlet_tables_match_oracle(k):
+    """Dirichlet kernel (reading A20): the residual patch matrix (outer
+    mesh-interior faces dropped) equals the oracle's assembled patch operator
+    minus its outer-face terms, and the padded eigenbasis solves the local
+    generalized eigenproblem on the kept nodes."""
+    from oracle import assemble, mesh
+    from oracle.smoother import PatchSmoother
+    np_ = 2 * (k + 1)
+    lv = mesh.Level(1, [4], 1.0)
+    A = assemble.assemble(lv, k)
+    S = PatchSmoother(lv, k, A, kernel="dirichlet")
+    P = mesh.patch_dofs(lv, [1, 2], k)
+    ref = A[P][:, P].toarray() - S._outer_face_terms(((False, False),))
+    LPR = ipmg.tables_1d(k, 16).reshape(np_, np_)
+    assert np.abs(LPR - ref).max() <= 1e-10 * np.abs(ref).max()
+    LP = ipmg.tables_1d(k, 3).reshape(np_, np_)
+    SD = ipmg.tables_1d(k, 20).reshape(np_, np_)
+    lam = ipmg.tables_1d(k, 24)
+    act = ipmg.tables_1d(k, 28)
+    assert act.sum() == np_ - 2
+    keep = np.arange(1, np_ - 1)
+    Mp = np.kron(np.eye(2), assemble.Reference(1, k).cell_matrices(1.0)[1])
+    for m in range(np_):
+        s = SD[:, m]
+        if act[m]:
+            assert abs(s[0]) + abs(s[-1]) == 0.0
+            res = LP[np.ix_(keep, keep)] @ s[keep] - lam[m] * Mp[np.ix_(keep, keep)] @ s[keep]
+            assert np.abs(res).max() <= 1e-9 * max(1.0, lam[m])
+            assert abs(s[keep] @ Mp[np.ix_(keep, keep)] @ s[keep] - 1.0) <= 1e-10
+    # [even | odd] ordering of the interior variant
+    h = np_ // 2
+    assert np.allclose(SD[::-1, :h], SD[:, :h], atol=1e-14) and np.allclose(SD[::-1, h:], -SD[:, h:], atol=1e-14)

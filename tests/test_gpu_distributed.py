@@ -285,3 +285,20 @@ def test_gmres_matches_serial():
         assert float(torch.linalg.norm(t.join(L, xs) - x) / torch.linalg.norm(x)) <= 1e-10
     finally:
         t.close()
+
+
+def test_dirichlet_smoother_bit_identical():
+    _need_gpu()
+    from paper_2405_18982_b200 import ipmg
+    t = Team(3, 2, 4, 2, None, kernel=ipmg.KERNEL_DIRICHLET)
+    try:
+        for level in range(1, t.nl):
+            n = t.serial.ndofs(level)
+            x, b = rand(n, 50 + level, torch.float32), rand(n, 60 + level, torch.float32)
+            xser = x.clone()
+            t.serial.smooth(level, xser, b)
+            xs, bs = t.split(level, x), t.split(level, b)
+            t.run(lambda r, h: h.smooth(level, xs[r], bs[r]))
+            assert torch.equal(t.join(level, xs), xser), "level %d" % level
+    finally:
+        t.close()

@@ -279,3 +279,73 @@ def test_gmres_solve(case, vprec):
     # a second solve reuses the library-owned Krylov basis
     res2 = h.gmres_solve(bl, x, rtol=1e-8, max_it=60)
     assert res2["iterations"] == res["iterations"]
+
+
+# ---------------------------------------------------------------- Dirichlet kernel (NEXT-1)
+@functools.lru_cache(maxsize=None)
+def handle_dir(dim, k, nl, coarse=None, vprec=1, post_reverse=1):
+    from paper_2405_18982_b200 import ipmg
+    return ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=vprec, kernel=ipmg.KERNEL_DIRICHLET,
+                       post_smooth_reverse=post_reverse)
+
+
+DIR_CASES = [(2, 1, 4, None), (2, 2, 4, None), (2, 3, 4, None), (2, 5, 3, None), (2, 7, 3, None),
+             (2, 3, 3, (2, 1)), (3, 1, 3, None), (3, 2, 3, None), (3, 3, 2, None), (3, 4, 2, None),
+             (3, 7, 2, None), (3, 2, 3, (2, 1, 2))]
+DIR_IDS = ["d%dk%dL%d%s" % (c[0], c[1], c[2], "" if c[3] is None else "c" + "".join(map(str, c[3]))) for c in DIR_CASES]
+
+
+@pytest.mark.parametrize("case", DIR_CASES, ids=DIR_IDS)
+def test_dirichlet_smoother_colours_and_step(case):
+    """Every colour of Algorithm 1 with the Dirichlet kernel (patch-only residual,
+    reduced local space) against the oracle's dense local solves of the
+    extracted A[V_j, V_j]; fp64 1e-12, fp32 1e-5 (on fp32-rounded inputs)."""
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle_dir(dim, k, nl, coarse)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    L = nl - 1
+    S = smoother.PatchSmoother(levels[L], k, ops[L], kernel="dirichlet")
+    x = uniform(ops[L].shape[0], seed=31)
+    b = uniform(ops[L].shape[0], seed=32)
+    for dtype, tol in ((torch.float64, 1e-12), (torch.float32, 1e-5)):
+        xr = np.asarray(torch.tensor(x, dtype=dtype).double())
+        br = np.asarray(torch.tensor(b, dtype=dtype).double())
+        xl, bl = to_lib(h, L, x, dtype), to_lib(h, L, b, dtype)
+        for c in range(2 ** dim):
+            out = torch.empty_like(xl)
+            h.smooth_colour(L, xl, bl, out, c)
+            assert rel(to_cw(h, L, out), S.colour_step_dirichlet(c, xr, br)) <= tol, (c, dtype)
+        out = torch.empty_like(xl)
+        h.smooth_colour(L, None, bl, out, 0)
+        assert rel(to_cw(h, L, out), S.colour_step_dirichlet(0, np.zeros_like(xr), br)) <= tol
+        for rev in (False, True):
+            xs = xl.clone()
+            h.smooth(L, xs, bl, reverse=rev)
+            assert rel(to_cw(h, L, xs), S.smooth(xr, br, reverse=rev)) <= tol, (rev, dtype)
+
+
+@pytest.mark.parametrize("case", [(2, 3, 4, None), (3, 2, 3, None), (3, 4, 2, None)], ids=["d2k3", "d3k2", "d3k4"])
+@pytest.mark.parametrize("vprec", [0, 1], ids=["fp64", "fp32"])
+def test_dirichlet_vcycle_and_gmres(case, vprec):
+    _need_gpu()
+    dim, k, nl, coarse = case
+    h = handle_dir(dim, k, nl, coarse, vprec)
+    levels, ops = oracle_levels(dim, k, nl, coarse)
+    L = nl - 1
+    V = multigrid.VCycle(dim, k, nl, n0=coarse, operators=ops, kernel="dirichlet",
+                         dtype=np.float64 if vprec == 0 else np.float32)
+    r = uniform(ops[L].shape[0], seed=33)
+    z = torch.empty(len(r), dtype=torch.float64, device="cuda")
+    h.vcycle(to_lib(h, L, r), z)
+    assert rel(to_cw(h, L, z), V(r)) <= (1e-12 if vprec == 0 else 1e-5)
+    b = assemble.rhs(levels[L], k)
+    xo, hist, conv = krylov.gmres(ops[L], b, V, rtol=1e-8)
+    bl = torch.empty(len(b), dtype=torch.float64, device="cuda")
+    h.rhs(L, bl)
+    x = torch.empty_like(bl)
+    res = h.gmres_solve(bl, x, rtol=1e-8, max_it=80)
+    assert res["converged"] and conv
+    assert abs(res["iterations"] - (len(hist) - 1)) <= 1
+    xg = to_cw(h, L, x)
+    assert np.linalg.norm(b - ops[L] @ xg) <= 1.5e-8 * np.linalg.norm(b)
