@@ -46,6 +46,11 @@ def main():
     res["vmult32_ms"] = timeit(lambda: h.vmult(L, x32, o32))
     res["restrict32_ms"] = timeit(lambda: h.residual_restrict(L, x32, b32, rc))
     res["prolong32_ms"] = timeit(lambda: h.prolongate_add(L, rc, o32))
+    hd = ipmg.Handle(dim, k, nl, vcycle_precision=ipmg.FP32, kernel=ipmg.KERNEL_DIRICHLET)
+    res["smooth_dir_c1_ms"] = timeit(lambda: hd.smooth_colour(L, x32, b32, o32, 1))
+    xs = x32.clone()
+    res["smooth_step_ms"] = timeit(lambda: h.smooth(L, xs, b32))
+    res["smooth_dir_step_ms"] = timeit(lambda: hd.smooth(L, xs, b32))
     b = torch.empty(n, dtype=torch.float64, device="cuda")
     h.rhs(L, b)
     sol = torch.empty_like(b)
@@ -55,6 +60,13 @@ def main():
         info.update(h.cg_solve(b, sol))
     res["solve_ms"] = timeit(solve, reps=5, warm=2)
     res["iterations"] = info["iterations"]
+
+    def gsolve(hh):
+        info.update(hh.gmres_solve(b, sol))
+    res["gmres_full_ms"] = timeit(lambda: gsolve(h), reps=3, warm=1)
+    res["gmres_full_its"] = info["iterations"]
+    res["gmres_dir_ms"] = timeit(lambda: gsolve(hd), reps=3, warm=1)
+    res["gmres_dir_its"] = info["iterations"]
     print(json.dumps(res), flush=True)
 
 

@@ -1,4 +1,4 @@
-"""The paper's Table 1 / Table 2-style fractional iteration counts on the GPU
+"""The paper's Table 1 / Table 2 (Dirichlet column) fractional iteration counts on the GPU
 (PAPER.md:284-300): 3D, full kernel, GMRES to 1e-8 preconditioned by the GMG
 V-cycle, f == 1, unit cube, reading A5 (row L = 2^L cells per direction).
 
@@ -26,6 +26,15 @@ for line in open(os.path.join(ROOT, "tests", "golden", "table1_full_kernel.txt")
                 TABLE1[(int(line[0]), 3 + j)] = float(v)
 
 
+TABLE2D = {}  # tests/golden/table2_dirichlet_clamped.txt, Dirichlet columns
+for line in open(os.path.join(ROOT, "tests", "golden", "table2_dirichlet_clamped.txt")):
+    line = line.split("#", 1)[0].split()
+    if line:
+        for j, v in enumerate(line[1:6]):
+            if v != "---":
+                TABLE2D[(int(line[0]), 3 + j)] = float(v)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--levels", default="2,3,4,5")
@@ -33,17 +42,20 @@ def main():
     ap.add_argument("--fp64", action="store_true")
     ap.add_argument("--forward-post", action="store_true", help="post-smoothing in forward colour order")
     ap.add_argument("--penalty", type=float, default=1.0, help="penalty_scale (reading A2 probe)")
+    ap.add_argument("--kernel", choices=["full", "dirichlet"], default="full")
     a = ap.parse_args()
     for L in [int(v) for v in a.levels.split(",")]:
         for k in [int(v) for v in a.degrees.split(",")]:
             h = ipmg.Handle(3, k, L, vcycle_precision=ipmg.FP64 if a.fp64 else ipmg.FP32,
-                            post_smooth_reverse=0 if a.forward_post else 1, penalty_scale=a.penalty)
+                            post_smooth_reverse=0 if a.forward_post else 1, penalty_scale=a.penalty,
+                            kernel=ipmg.KERNEL_DIRICHLET if a.kernel == "dirichlet" else ipmg.KERNEL_FULL)
             n = h.ndofs(L - 1)
             b = torch.empty(n, dtype=torch.float64, device="cuda")
             h.rhs(L - 1, b)
             x = torch.empty_like(b)
             r = h.gmres_solve(b, x, rtol=1e-8, max_it=100)
-            print(json.dumps({"L": L, "k": k, "dofs": n, "nu": r["nu"], "paper": TABLE1.get((L, k)),
+            paper = TABLE1.get((L, k)) if a.kernel == "full" else TABLE2D.get((L, k))
+            print(json.dumps({"L": L, "k": k, "dofs": n, "nu": r["nu"], "paper": paper, "kernel": a.kernel,
                               "iterations": r["iterations"], "converged": r["converged"],
                               "vcycle": "fp64" if a.fp64 else "fp32", "post": "forward" if a.forward_post else "reverse",
                               "penalty_scale": a.penalty}),
