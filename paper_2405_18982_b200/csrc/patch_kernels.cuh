@@ -98,10 +98,13 @@ constexpr int bank_cost(F base, int nthreads) {
 
 template <int D, typename T>
 struct Cfg {
-#ifndef IPMG_R32
-#define IPMG_R32 2
+  // lines per thread: fp32 2 for k <= 3, 1 for k >= 4 (C3 sweep: 3D k=4/5 smoother
+  // +10 %, 2D k=7 solve 30.4 -> 29.2 ms); fp64 1
+#ifdef IPMG_R32
+  static constexpr int R = sizeof(T) == 4 ? IPMG_R32 : 1;
+#else
+  static constexpr int R = (sizeof(T) == 4 && NC <= 4) ? 2 : 1;
 #endif
-  static constexpr int R = sizeof(T) == 4 ? IPMG_R32 : 1;     // lines per thread
   static constexpr int RP = NP + 1;                           // row pitch (odd)
   static constexpr int NL = (D == 2) ? NP : NP * NP;          // lines per direction per patch
   static constexpr int G = NL / R;                            // line groups per patch
@@ -113,10 +116,12 @@ struct Cfg {
 #ifndef IPMG_GROUPS_TARGET
 #define IPMG_GROUPS_TARGET 32
 #endif
-  // line groups per CTA: 1 warp (measured best for k >= 3); 4 warps for k <= 2,
+  // line groups per CTA: 1 warp (measured best for k >= 3; 2 warps for fp32 with
+  // R = 1); 4 warps for k <= 2,
   // whose tiny patches otherwise leave a CTA with too little work (C3 sweep: 3D
   // k=2 smoother step 10.4 -> 12.7 GDoF/s)
-  static constexpr int GT = NC <= 3 ? 4 * IPMG_GROUPS_TARGET : IPMG_GROUPS_TARGET;
+  static constexpr int GT = NC <= 3 ? 4 * IPMG_GROUPS_TARGET
+                                    : ((sizeof(T) == 4 && R == 1) ? 2 * IPMG_GROUPS_TARGET : IPMG_GROUPS_TARGET);
   static constexpr int PPC = (GT / G) > 1 ? (GT / G) : 1;   // patches per CTA
   static constexpr int GROUPS = PPC * G;
   static constexpr int NT = (((GROUPS + 31) / 32) * 32) > 256 ? 256 : ((GROUPS + 31) / 32) * 32;
