@@ -183,7 +183,20 @@ struct Cfg {
     return best;
   }
   static constexpr int FARR = pick_farr();
-  static constexpr int FSZ = 4 * D * FARR;                     // face scratch per patch
+  // face scratch per patch, padded so that the face-injection reads of the
+  // patches sharing a warp (lane u -> patch u / G, line u % G) hit distinct banks
+  static constexpr int fpos_c(int t) { return D == 2 ? t : (t % NP) + (t / NP) * FROW; }
+  static constexpr int pick_fsz() {
+    const int base = 4 * D * FARR;
+    int best = base, bc = 1 << 30;
+    for (int pad = 0; pad < 32; ++pad) {
+      struct B { int fs; constexpr int operator()(int u) const { return (u / G) * fs + fpos_c(u % G); } };
+      const int c = bank_cost<T>(B{base + pad}, 32);
+      if (c < bc) { bc = c; best = base + pad; }
+    }
+    return best;
+  }
+  static constexpr int FSZ = pick_fsz();
   // neighbour-cell staging (cp.async prefetch at kernel start): one slot per
   // face-neighbour cell, slot pitch SP a multiple of 16 bytes with SP/VE odd so
   // that the 16-byte row reads of neighbouring slots hit different banks
@@ -764,6 +777,12 @@ template <int D>
 __device__ __forceinline__ int fidx(int p, int a, int s, int kind) {
   return ((p * D + a) * 2 + s) * 2 + kind;
 }
+// element offset of face array (a, s, kind) of patch p (patch pitch FSZ)
+template <int D, typename T>
+__device__ __forceinline__ int fofs(int p, int a, int s, int kind) {
+  using C = Cfg<D, T>;
+  return p * C::FSZ + ((a * 2 + s) * 2 + kind) * C::FARR;
+}
 
 // position of tangential point t inside a face array
 template <int D, typename T>
@@ -886,8 +905,8 @@ __device__ __forceinline__ void trace_unit(T* F, const T* __restrict__ x, const 
       du[i] = out2[1][i];
     }
   }
-  T* fu = F + fidx<D>(p, A, s, 0) * C::FARR;
-  T* fd = F + fidx<D>(p, A, s, 1) * C::FARR;
+  T* fu = F + fofs<D, T>(p, A, s, 0);
+  T* fd = F + fofs<D, T>(p, A, s, 1);
 #pragma unroll
   for (int lb = 0; lb < NC; ++lb) {
     const int pos = fpos<D, T>(h * NC + lb + NP * ic);
@@ -944,7 +963,7 @@ __device__ __forceinline__ void face_transform(T* F, const PInfo<D>* pis, int np
       const int o = e % nl, arr = e / nl;         // arr = fidx(p, a, s, kind)
       const int a = (arr / 4) % D, p = arr / (4 * D);
       if (face_mode<SMOOTHER>(a, first_tan(a)) != 2) continue;
-      T* base = F + arr * C::FARR + (D == 2 ? 0 : o * C::FROW);
+      T* base = F + p * C::FSZ + (arr % (4 * D)) * C::FARR + (D == 2 ? 0 : o * C::FROW);
       face_line<T>(base, 1, 2, pis[p].var[first_tan(a)]);
     }
     __syncthreads();
@@ -957,7 +976,7 @@ __device__ __forceinline__ void face_transform(T* F, const PInfo<D>* pis, int np
       const int b = second_tan(a);
       const int mode = face_mode<SMOOTHER>(a, b);
       if (mode == 0) continue;
-      T* base = F + arr * C::FARR + o;
+      T* base = F + p * C::FSZ + (arr % (4 * D)) * C::FARR + o;
       face_line<T>(base, C::FROW, mode, pis[p].var[b]);
     }
     __syncthreads();
@@ -989,8 +1008,8 @@ __device__ __forceinline__ void face_inject(T (&y)[R][NP], const T* F, int p, in
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int pos = fpos<D, T>(g + r * C::G);
-    const T ul = F[fidx<D>(p, a, 0, 0) * C::FARR + pos], dl = F[fidx<D>(p, a, 0, 1) * C::FARR + pos];
-    const T uh = F[fidx<D>(p, a, 1, 0) * C::FARR + pos], dh = F[fidx<D>(p, a, 1, 1) * C::FARR + pos];
+    const T ul = F[fofs<D, T>(p, a, 0, 0) + pos], dl = F[fofs<D, T>(p, a, 0, 1) + pos];
+    const T uh = F[fofs<D, T>(p, a, 1, 0) + pos], dh = F[fofs<D, T>(p, a, 1, 1) + pos];
     const T sg = T(SGN);
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
