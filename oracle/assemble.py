@@ -32,15 +32,15 @@ def _kron_all(mats):
 class Reference:
     """Reference-cell tables for degree k in dimension d (unit cell [0,1]^d)."""
 
-    def __init__(self, dim, k, nq=None):
+    def __init__(self, dim, k, nq=None, kind="lagrange"):
         self.dim, self.k = dim, k
         self.nc = k + 1
         self.nodes = basis.gll_nodes(self.nc)
         nq = nq if nq is not None else k + 1         # exact for degree 2k (A3)
         self.qx, self.qw = basis.gauss(nq)
-        self.V, self.D = basis.lagrange(self.nodes, self.qx)       # (nq, nc)
-        self.V0, self.D0 = basis.lagrange(self.nodes, [0.0])       # (1, nc)
-        self.V1, self.D1 = basis.lagrange(self.nodes, [1.0])
+        self.V, self.D = basis.evaluate(kind, k, self.qx)        # (nq, nc)
+        self.V0, self.D0 = basis.evaluate(kind, k, [0.0])        # (1, nc)
+        self.V1, self.D1 = basis.evaluate(kind, k, [1.0])
 
     def cell_matrices(self, h):
         """Cell stiffness K_ij = int_K grad phi_i . grad phi_j and mass, by
@@ -112,11 +112,12 @@ def _cell_grid(level):
     return grids, lin
 
 
-def assemble(level: Level, k, penalty_scale=1.0):
+def assemble(level: Level, k, penalty_scale=1.0, kind="lagrange"):
     """Global SIPG matrix of ``level`` in cell-wise lexicographic numbering, CSR.
-    Exact zeros (e.g. phi_i(0) = 0 for i != 0 on GLL nodes) are not stored."""
+    Exact zeros (e.g. phi_i(0) = 0 for i != 0 on GLL nodes) are not stored.
+    kind: 1D basis ('lagrange' GLL, or 'hermite' for the clamped kernel)."""
     d, h = level.dim, level.h
-    ref = Reference(d, k)
+    ref = Reference(d, k, kind=kind)
     nloc = ref.nc ** d
     gamma = basis.penalty(k, h, h, penalty_scale)
     rows, cols, vals = [], [], []
@@ -168,12 +169,12 @@ def interpolate(level: Level, k, u):
     return u(cell_nodes(level, k))
 
 
-def rhs(level: Level, k, f=None, nq=None):
+def rhs(level: Level, k, f=None, nq=None, kind="lagrange"):
     """b_i = int f phi_i (eq. weak_form) by tensor Gauss
     quadrature with k+3 points per direction; f=None means f == 1
     (PAPER.md:331)."""
     d, h = level.dim, level.h
-    ref = Reference(d, k, nq=nq if nq is not None else k + 3)
+    ref = Reference(d, k, nq=nq if nq is not None else k + 3, kind=kind)
     Phi = _kron_all([ref.V] * d)
     w = np.diag(_kron_all([np.diag(ref.qw)] * d)) * h ** d
     nq1 = len(ref.qx)

@@ -57,3 +57,69 @@ def penalty(k, h_minus, h_plus, scale=1.0):
     sides take the cell's own h (reading A2).  SPEC.md:159 worked
     example: k=2, h=1/4 -> 48."""
     return scale * k * (k + 1) * (1.0 / h_plus + 1.0 / h_minus)
+
+
+# ---------------------------------------------------------------- Hermite-type basis
+# (clamped kernel, PAPER.md:226-231, Fig. 3 right; SURVEY.md NEXT-3; reading A19)
+def hermite_points(k):
+    """Interior interpolation points of the Hermite-type basis: the k-3 Gauss
+    points on (0,1)."""
+    return gauss(k - 3)[0] if k > 3 else np.zeros(0)
+
+
+def hermite(k, x):
+    """Values V[q, j] and derivatives D[q, j] of the Hermite-type basis of Q_k
+    (k >= 3): the dual basis of the functionals
+        l_0 = v(0), l_1 = v'(0), l_{1+m} = v(eta_m) (m < k-3), l_{k-1} = -v'(1), l_k = v(1)
+    (value and derivative at both ends, Lagrange at the interior Gauss points;
+    the sign of v'(1) makes the reflection x -> 1-x map psi_j to psi_{k-j}).
+    Built by inverting the functional matrix in the shifted Legendre basis."""
+    if k < 3:
+        raise ValueError("the Hermite-type basis needs k >= 3")
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    eta = hermite_points(k)
+    n = k + 1
+    F = np.zeros((n, n))
+    for m in range(n):
+        c = np.zeros(m + 1)
+        c[m] = 1.0
+        dc = npleg.legder(c) if m > 0 else np.zeros(1)
+        F[0, m] = npleg.legval(-1.0, c)
+        F[1, m] = 2.0 * npleg.legval(-1.0, dc)
+        for i, e in enumerate(eta):
+            F[2 + i, m] = npleg.legval(2.0 * e - 1.0, c)
+        F[k - 1, m] = -2.0 * npleg.legval(1.0, dc)
+        F[k, m] = npleg.legval(1.0, c)
+    C = np.linalg.inv(F)                      # psi_j = sum_m C[m, j] P_m(2x - 1)
+    V = np.zeros((len(x), n))
+    D = np.zeros((len(x), n))
+    for m in range(n):
+        c = np.zeros(m + 1)
+        c[m] = 1.0
+        pm = npleg.legval(2.0 * x - 1.0, c)
+        dpm = 2.0 * npleg.legval(2.0 * x - 1.0, npleg.legder(c)) if m > 0 else np.zeros_like(x)
+        V += np.outer(pm, C[m])
+        D += np.outer(dpm, C[m])
+    return V, D
+
+
+def evaluate(kind, k, x):
+    """(V, D) of the 1D basis `kind` ('lagrange': GLL Lagrange, 'hermite')."""
+    if kind == "hermite":
+        return hermite(k, x)
+    return lagrange(gll_nodes(k + 1), x)
+
+
+def child_matrix(kind, k, q):
+    """1D embedding of the coarse basis into child q in {0, 1}: B[i, j] = l_i(psi_j
+    restricted to the child), l_i the child's defining functionals (nodal values
+    for Lagrange; values/derivatives as in `hermite` for Hermite; a child
+    derivative is 1/2 of the coarse one)."""
+    if kind == "lagrange":
+        nodes = gll_nodes(k + 1)
+        return lagrange(nodes, (nodes + q) / 2.0)[0]
+    eta = hermite_points(k)
+    V0, D0 = hermite(k, [q / 2.0])
+    V1, D1 = hermite(k, [(1.0 + q) / 2.0])
+    Vi = hermite(k, (eta + q) / 2.0)[0] if k > 3 else np.zeros((0, k + 1))
+    return np.vstack([V0, 0.5 * D0, Vi, -0.5 * D1, V1])

@@ -16,6 +16,11 @@ PAPER.md:257; reading A9).  Post-smoothing may visit colours in reverse
 Additive (BASELINE.json configs[4]; not in the paper): x <- x + omega sum_j
 R_j^T A_j^{-1} R_j (b - A x), omega = 1/2^d by default (reading A17).
 
+Clamped kernel (NEXT-3, reading A19): the same update on the
+Hermite-type basis (oracle/basis.hermite) with V_j = patch functions whose value
+and normal derivative vanish on the mesh-interior patch faces ((2k-2)^d dofs);
+the patch-only residual is then exact (pinned: A[V_j, outside] = 0).
+
 Dirichlet kernel (reading A20): V_j = the
 patch dofs whose node index is not on a patch-boundary face that is a
 mesh-interior face (omitting "the functions associated to boundary
@@ -32,7 +37,7 @@ import scipy.linalg as sla
 from . import mesh
 
 
-def interior_mask(dim, k, signature=None):
+def interior_mask(dim, k, signature=None, width=1):
     """Dirichlet-kernel subspace inside the patch-lexicographic ordering: True
     unless some direction's node index lies on a patch-boundary face that is a
     MESH-INTERIOR face (index 0 or 2k+1).  Nodes on the domain boundary stay
@@ -46,7 +51,7 @@ def interior_mask(dim, k, signature=None):
         rem = lex
         for a in range(dim):
             i = rem % npatch
-            if (i == 0 and not sig[a][0]) or (i == npatch - 1 and not sig[a][1]):
+            if (i < width and not sig[a][0]) or (i >= npatch - width and not sig[a][1]):
                 m[lex] = False
             rem //= npatch
     return m
@@ -69,11 +74,17 @@ class PatchSmoother:
             grp = []
             for key, idxs in bysig.items():
                 idx = np.array(idxs)
-                if kernel == "dirichlet":
+                if kernel in ("dirichlet", "clamped"):
                     assert cache_by_signature
-                    mask = interior_mask(level.dim, k, key)
+                    # clamped (Hermite-type basis): V_j drops value AND
+                    # derivative functions at mesh-interior patch faces (width 2); for
+                    # those test functions every outer face term vanishes, so the
+                    # assembled rows are already the exact patch-local residual
+                    mask = interior_mask(level.dim, k, key, 2 if kernel == "clamped" else 1)
                     iI = idx[:, mask]
-                    APP = self.A[idx[0]][:, idx[0]].toarray() - self._outer_face_terms(key).astype(self.dtype)
+                    APP = self.A[idx[0]][:, idx[0]].toarray()
+                    if kernel == "dirichlet":
+                        APP = APP - self._outer_face_terms(key).astype(self.dtype)
                     AIP = APP[mask, :]                            # patch operator, rows V_j
                     AII = AIP[:, mask]                            # = A[V_j, V_j] (checked by the pins)
                     grp.append((sla.lu_factor(AII), iI, idx, AIP))
@@ -147,7 +158,7 @@ class PatchSmoother:
         x = np.array(x, dtype=self.dtype)
         b = np.asarray(b, dtype=self.dtype)
         order = range(self.ncolours - 1, -1, -1) if reverse else range(self.ncolours)
-        if self.kernel == "dirichlet":
+        if self.kernel in ("dirichlet", "clamped"):
             for c in order:
                 x = self.colour_step_dirichlet(c, x, b)
             return x

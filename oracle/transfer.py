@@ -14,7 +14,7 @@ from . import basis
 from .mesh import Level
 
 
-def prolongation(coarse: Level, fine: Level, k):
+def prolongation(coarse: Level, fine: Level, k, kind="lagrange"):
     """Sparse P (fine ndofs x coarse ndofs), cell-wise lexicographic numbering on
     both levels.  Built by evaluating every coarse basis function at every
     fine-child node (definition of the embedding)."""
@@ -23,7 +23,14 @@ def prolongation(coarse: Level, fine: Level, k):
     nodes = basis.gll_nodes(nc)
     nloc = nc ** d
     blocks = {}
-    for q in itertools.product((0, 1), repeat=d):
+    if kind == "hermite":   # tensor product of the 1D child embeddings (basis.child_matrix)
+        B1 = [basis.child_matrix(kind, k, q) for q in (0, 1)]
+        for q in itertools.product((0, 1), repeat=d):
+            B = np.ones((1, 1))
+            for i in range(d):              # x fastest: later factors are slower
+                B = np.kron(B1[q[i]], B)
+            blocks[q] = B
+    for q in ([] if kind == "hermite" else itertools.product((0, 1), repeat=d)):
         # fine node coordinates (in the coarse reference cell) of child q
         pts = np.array([[(nodes[(l // nc ** i) % nc] + q[i]) / 2.0 for i in range(d)]
                         for l in range(nloc)])
