@@ -56,7 +56,16 @@ typedef enum { IPMG_FP64 = 0, IPMG_FP32 = 1 } ipmg_precision;
  * dofs, exact residual from the face neighbours); DIRICHLET = PAPER.md:212-225
  * (V_j without the outer nodes at mesh-interior patch faces, residual from the
  * patch cells only -- inconsistent, use GMRES; reading A20). */
-typedef enum { IPMG_KERNEL_FULL = 0, IPMG_KERNEL_DIRICHLET = 1 } ipmg_kernel;
+typedef enum { IPMG_KERNEL_FULL = 0, IPMG_KERNEL_DIRICHLET = 1, IPMG_KERNEL_CLAMPED = 2 } ipmg_kernel;
+/* CLAMPED = PAPER.md:226-231: V_j = patch functions with zero value and normal
+ * derivative on the mesh-interior patch faces ((2k-2)^d dofs), exact residual
+ * from the patch cells only; requires the Hermite-type basis. */
+
+/* 1D basis of Q_k on every level: GLL Lagrange or the
+ * Hermite-type basis of the clamped kernel (dual to v(0), v'(0), v at the k-3
+ * interior Gauss points, -v'(1), v(1); k >= 3; reading A19).  All
+ * vectors are coefficient vectors in the chosen basis. */
+typedef enum { IPMG_BASIS_LAGRANGE = 0, IPMG_BASIS_HERMITE = 1 } ipmg_basis;
 
 /* Multiplicative = Algorithm 1; additive = BASELINE.json
  * configs[4] (damped, omega default 1/2^d, reading A17). */
@@ -87,6 +96,7 @@ typedef struct {
   int device;               /* CUDA device ordinal                                         */
   void *cuda_stream;        /* cudaStream_t all work is enqueued on                        */
   ipmg_comm *comm;          /* NULL: one GPU; else this rank's communicator (not owned)    */
+  int basis;                /* ipmg_basis; CLAMPED needs HERMITE, DIRICHLET needs LAGRANGE */
 } ipmg_config;
 
 typedef struct ipmg_handle ipmg_handle;

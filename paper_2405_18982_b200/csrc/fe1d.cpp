@@ -265,9 +265,42 @@ bool gen_eig(int n, const std::vector<double>& L, const std::vector<double>& M,
   return true;
 }
 
-FE1D build_fe1d(int k, double penalty_scale) {
+// Gauss-Jordan inverse of a small dense matrix (row-major); false if singular
+static bool invert(int n, std::vector<double> A, std::vector<double>& Ai) {
+  Ai.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) Ai[i * n + i] = 1.0;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(A[r * n + c]) > std::fabs(A[piv * n + c])) piv = r;
+    if (std::fabs(A[piv * n + c]) < 1e-300) return false;
+    for (int j = 0; j < n; ++j) {
+      std::swap(A[c * n + j], A[piv * n + j]);
+      std::swap(Ai[c * n + j], Ai[piv * n + j]);
+    }
+    const double inv = 1.0 / A[c * n + c];
+    for (int j = 0; j < n; ++j) {
+      A[c * n + j] *= inv;
+      Ai[c * n + j] *= inv;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = A[r * n + c];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        A[r * n + j] -= f * A[c * n + j];
+        Ai[r * n + j] -= f * Ai[c * n + j];
+      }
+    }
+  }
+  return true;
+}
+
+FE1D build_fe1d(int k, double penalty_scale, int basis, int dir_width) {
   FE1D fe;
   fe.k = k;
+  fe.basis = basis;
+  fe.dir_width = dir_width;
   fe.nc = k + 1;
   fe.np = 2 * fe.nc;
   const int nc = fe.nc, np = fe.np;
@@ -290,6 +323,49 @@ FE1D build_fe1d(int k, double penalty_scale) {
     for (int j = 0; j < nc; ++j) fe.w[i] += fe.M[i * nc + j];
   lagrange(fe.nodes, 0.0, v, fe.d0);
   lagrange(fe.nodes, 1.0, v, fe.d1);
+  // Hermite-type basis (clamped kernel, reading A19): the dual
+  // basis of {v(0), v'(0), v(eta_1..eta_{k-3}), -v'(1), v(1)}, eta = interior Gauss
+  // points.  With F[i][n] = l_i(phi_n) (functionals on the GLL Lagrange basis),
+  // psi_j = sum_n T[n][j] phi_n with T = F^{-1}, i.e. T[i][j] = psi_j(xi_i); every
+  // table below is the Lagrange one transformed by T (exact).
+  std::vector<double> T, F;
+  if (basis == 1) {
+    F.assign(nc * nc, 0.0);
+    std::vector<double> eta, ew;
+    if (k > 3) gauss(k - 3, eta, ew);
+    for (int n = 0; n < nc; ++n) {
+      F[0 * nc + n] = n == 0 ? 1.0 : 0.0;
+      F[1 * nc + n] = fe.d0[n];
+      F[(k - 1) * nc + n] = -fe.d1[n];
+      F[k * nc + n] = n == k ? 1.0 : 0.0;
+    }
+    for (int m = 0; m < k - 3; ++m) {
+      lagrange(fe.nodes, eta[m], v, d);
+      for (int n = 0; n < nc; ++n) F[(2 + m) * nc + n] = v[n];
+    }
+    invert(nc, F, T);
+    auto tt = [&](const std::vector<double>& A) {   // T^T A T
+      std::vector<double> B(nc * nc, 0.0), C(nc * nc, 0.0);
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < nc; ++j)
+          for (int p = 0; p < nc; ++p) B[i * nc + j] += A[i * nc + p] * T[p * nc + j];
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < nc; ++j)
+          for (int p = 0; p < nc; ++p) C[i * nc + j] += T[p * nc + i] * B[p * nc + j];
+      return C;
+    };
+    auto tv = [&](const std::vector<double>& a) {   // T^T a
+      std::vector<double> b(nc, 0.0);
+      for (int j = 0; j < nc; ++j)
+        for (int p = 0; p < nc; ++p) b[j] += T[p * nc + j] * a[p];
+      return b;
+    };
+    fe.M = tt(fe.M);
+    fe.K = tt(fe.K);
+    fe.w = tv(fe.w);
+    fe.d0 = tv(fe.d0);
+    fe.d1 = tv(fe.d1);
+  }
   fe.MP = block_mass(fe, 2);
   for (int var = 0; var < 4; ++var) {
     fe.LP[var] = sipg_chain(fe, 2, var & 1, var & 2);
@@ -330,10 +406,11 @@ FE1D build_fe1d(int k, double penalty_scale) {
   fe.even_odd_dir = false;
   for (int var = 0; var < 4; ++var) {
     const bool lo_b = var & 1, hi_b = var & 2;
+    const int wd = dir_width;   // 1 Dirichlet (Lagrange), 2 clamped (Hermite: value + derivative)
     fe.LPR[var] = sipg_chain_modes(fe, 2, lo_b ? 1 : 2, hi_b ? 1 : 2);
     std::vector<int> keep;
     for (int i = 0; i < np; ++i)
-      if (!((i == 0 && !lo_b) || (i == np - 1 && !hi_b))) keep.push_back(i);
+      if (!((i < wd && !lo_b) || (i >= np - wd && !hi_b))) keep.push_back(i);
     const int nk = (int)keep.size();
     std::vector<double> Lk(nk * nk), Mk(nk * nk), Sk, lk;
     for (int a = 0; a < nk; ++a)
@@ -363,10 +440,12 @@ FE1D build_fe1d(int k, double penalty_scale) {
       for (int h = 0; h < 2; ++h) {
         const int base = h * (np / 2);
         const double sg = h == 0 ? 1.0 : -1.0;
-        S[0 * np + base] = r2;
-        S[(np - 1) * np + base] = sg * r2;
+        for (int q = 0; q < wd; ++q) {   // inactive boundary pairs (e_q +- e_{np-1-q}) / sqrt2
+          S[q * np + base + q] = r2;
+          S[(np - 1 - q) * np + base + q] = sg * r2;
+        }
         for (int q = 0; q < nk / 2; ++q) {
-          const int m = h == 0 ? ev[q] : od[q], col = base + 1 + q;
+          const int m = h == 0 ? ev[q] : od[q], col = base + wd + q;
           fe.lamD[var][col] = lk[m];
           fe.actD[var][col] = 1.0;
           for (int a = 0; a < nk / 2; ++a) {   // exact symmetrisation
@@ -393,6 +472,18 @@ FE1D build_fe1d(int k, double penalty_scale) {
     double x = 0.5 * (fe.nodes[i % nc] + (i / nc));
     lagrange(fe.nodes, x, v, d);
     for (int j = 0; j < nc; ++j) fe.P[i * nc + j] = v[j];
+  }
+  if (basis == 1) {   // P_H (child c) = F P_L(child c) T
+    std::vector<double> PH(np * nc, 0.0);
+    for (int c = 0; c < 2; ++c)
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < nc; ++j) {
+          double acc = 0.0;
+          for (int p = 0; p < nc; ++p)
+            for (int q = 0; q < nc; ++q) acc += F[i * nc + p] * fe.P[(c * nc + p) * nc + q] * T[q * nc + j];
+          PH[(c * nc + i) * nc + j] = acc;
+        }
+    fe.P = PH;
   }
   return fe;
 }

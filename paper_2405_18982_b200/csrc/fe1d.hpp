@@ -18,6 +18,8 @@ namespace ipmg {
 
 struct FE1D {
   int k = 0, nc = 0, np = 0;       // degree, nodes per cell, nodes per 2-cell patch
+  int basis = 0;                   // 0 GLL Lagrange, 1 Hermite-type (clamped kernel, reading A19)
+  int dir_width = 1;               // nodes dropped per mesh-interior patch side: 1 Dirichlet, 2 clamped
   double gamma = 0;                // unit-h penalty 2k(k+1)*scale (reading A2)
   std::vector<double> nodes;       // GLL nodes on [0,1]                       (nc)
   std::vector<double> w;           // int_0^1 phi_i                             (nc)
@@ -41,8 +43,10 @@ struct FE1D {
   bool even_odd_dir = false;
 };
 
-// Build all unit tables for degree k (1..7); penalty_scale multiplies gamma.
-FE1D build_fe1d(int k, double penalty_scale);
+// Build all unit tables for degree k (1..7); penalty_scale multiplies gamma;
+// basis 1 = Hermite-type (k >= 3); dir_width: reduced-space width of the
+// Dirichlet/clamped tables.
+FE1D build_fe1d(int k, double penalty_scale, int basis = 0, int dir_width = 1);
 
 // Global 1D SIPG matrix (unit h) on ncell cells with boundary faces at both ends
 // and its mass; row-major (ncell*nc)^2.  Used for the coarse solve (reading A10).

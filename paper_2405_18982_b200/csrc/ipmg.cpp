@@ -232,8 +232,7 @@ struct ipmg_handle {
   ipmg_status smooth_colour(int level, int prec, const void* xi, const void* b, void* xo, int colour) {
     return run(KC_SMOOTH, level, smooth_bytes(level, prec, colour, xi != nullptr), 1,
                [&] {
-                 return (cfg.kernel == IPMG_KERNEL_DIRICHLET ? ksd : ks).smooth(dim, prec, xi, b, xo, geom[level], colour,
-                                                                                stream);
+                 return (cfg.kernel != IPMG_KERNEL_FULL ? ksd : ks).smooth(dim, prec, xi, b, xo, geom[level], colour, stream);
                },
                "smooth_colour");
   }
@@ -403,6 +402,7 @@ void ipmg_config_default(ipmg_config* c) {
   c->post_smooth_reverse = 1;
   c->vcycle_precision = IPMG_FP32;
   c->penalty_scale = 1.0;
+  c->basis = IPMG_BASIS_LAGRANGE;
   c->device = 0;
   c->cuda_stream = nullptr;
 }
@@ -445,12 +445,22 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
       g_create_error = "coarse_cells must be 1 or 2 per direction";
       return IPMG_ERR_INVALID_ARG;
     }
-  if (cfg->kernel != IPMG_KERNEL_FULL && cfg->kernel != IPMG_KERNEL_DIRICHLET) {
-    g_create_error = "kernel must be IPMG_KERNEL_FULL or IPMG_KERNEL_DIRICHLET";
+  if (cfg->kernel != IPMG_KERNEL_FULL && cfg->kernel != IPMG_KERNEL_DIRICHLET && cfg->kernel != IPMG_KERNEL_CLAMPED) {
+    g_create_error = "kernel must be IPMG_KERNEL_FULL, _DIRICHLET or _CLAMPED";
     return IPMG_ERR_UNSUPPORTED;
   }
-  if (cfg->kernel == IPMG_KERNEL_DIRICHLET && cfg->smoother != IPMG_MULTIPLICATIVE) {
-    g_create_error = "the Dirichlet kernel is a multiplicative smoother (Algorithm 1)";
+  if (cfg->kernel != IPMG_KERNEL_FULL && cfg->smoother != IPMG_MULTIPLICATIVE) {
+    g_create_error = "the Dirichlet and clamped kernels are multiplicative smoothers (Algorithm 1)";
+    return IPMG_ERR_UNSUPPORTED;
+  }
+  if (cfg->basis != IPMG_BASIS_LAGRANGE && cfg->basis != IPMG_BASIS_HERMITE) {
+    g_create_error = "unknown basis";
+    return IPMG_ERR_INVALID_ARG;
+  }
+  if ((cfg->kernel == IPMG_KERNEL_CLAMPED && cfg->basis != IPMG_BASIS_HERMITE) ||
+      (cfg->kernel == IPMG_KERNEL_DIRICHLET && cfg->basis != IPMG_BASIS_LAGRANGE) ||
+      (cfg->basis == IPMG_BASIS_HERMITE && cfg->degree < 3)) {
+    g_create_error = "clamped kernel needs the Hermite-type basis, Dirichlet the Lagrange one; Hermite needs k >= 3";
     return IPMG_ERR_UNSUPPORTED;
   }
   if (cfg->smoother != IPMG_MULTIPLICATIVE && cfg->smoother != IPMG_ADDITIVE) {
@@ -482,7 +492,7 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   };
   if (cudaSetDevice(cfg->device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return bail(IPMG_ERR_CUDA); }
   // ---- 1D tables and their upload
-  h->fe = ipmg::build_fe1d(h->k, h->cfg.penalty_scale);
+  h->fe = ipmg::build_fe1d(h->k, h->cfg.penalty_scale, cfg->basis, cfg->kernel == IPMG_KERNEL_CLAMPED ? 2 : 1);
   if (!h->fe.even_odd) {   // the interior-patch fast path relies on the reflection symmetry
     h->err = "interior patch eigenvectors are not even/odd";
     return bail(IPMG_ERR_UNSUPPORTED);
@@ -492,7 +502,7 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
     ipmg_status st = h->cuda(h->ks.upload(h->fe), "table upload");
     if (st != IPMG_OK) return bail(st);
   }
-  if (cfg->kernel == IPMG_KERNEL_DIRICHLET) {
+  if (cfg->kernel == IPMG_KERNEL_DIRICHLET || cfg->kernel == IPMG_KERNEL_CLAMPED) {
     if (!h->fe.even_odd_dir) {
       h->err = "Dirichlet interior eigenvectors are not even/odd";
       return bail(IPMG_ERR_UNSUPPORTED);

@@ -17,7 +17,8 @@ IPMG_OK = 0
 IPMG_ERR_NOT_CONVERGED = 7
 FP64, FP32 = 0, 1
 MULTIPLICATIVE, ADDITIVE = 0, 1
-KERNEL_FULL, KERNEL_DIRICHLET = 0, 1
+KERNEL_FULL, KERNEL_DIRICHLET, KERNEL_CLAMPED = 0, 1, 2
+BASIS_LAGRANGE, BASIS_HERMITE = 0, 1
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "SIZE_MISMATCH", 4: "OUT_OF_MEMORY",
           5: "CUDA", 6: "NCCL", 7: "NOT_CONVERGED"}
 
@@ -38,7 +39,7 @@ class Config(ctypes.Structure):
                 ("smoother", ctypes.c_int), ("additive_omega", ctypes.c_double),
                 ("post_smooth_reverse", ctypes.c_int), ("vcycle_precision", ctypes.c_int),
                 ("penalty_scale", ctypes.c_double), ("device", ctypes.c_int),
-                ("cuda_stream", ctypes.c_void_p), ("comm", ctypes.c_void_p)]
+                ("cuda_stream", ctypes.c_void_p), ("comm", ctypes.c_void_p), ("basis", ctypes.c_int)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -191,7 +192,7 @@ class Handle:
 
     def __init__(self, dim, degree, n_levels, coarse_cells=None, h0=0.5, smoother=MULTIPLICATIVE,
                  additive_omega=0.0, post_smooth_reverse=1, vcycle_precision=FP32, penalty_scale=1.0,
-                 device=0, stream=None, comm=None, kernel=KERNEL_FULL):
+                 device=0, stream=None, comm=None, kernel=KERNEL_FULL, basis=None):
         import torch
         self.lib = load()
         cfg = Config()
@@ -204,6 +205,8 @@ class Handle:
         cfg.post_smooth_reverse, cfg.vcycle_precision = post_smooth_reverse, vcycle_precision
         cfg.penalty_scale, cfg.device = penalty_scale, device
         cfg.kernel = kernel
+        # the clamped kernel lives on the Hermite-type basis (the whole hierarchy)
+        cfg.basis = (BASIS_HERMITE if kernel == KERNEL_CLAMPED else BASIS_LAGRANGE) if basis is None else basis
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
