@@ -26,13 +26,16 @@ for line in open(os.path.join(ROOT, "tests", "golden", "table1_full_kernel.txt")
                 TABLE1[(int(line[0]), 3 + j)] = float(v)
 
 
-TABLE2D = {}  # tests/golden/table2_dirichlet_clamped.txt, Dirichlet columns
+TABLE2D, TABLE2C = {}, {}   # tests/golden/table2_dirichlet_clamped.txt
 for line in open(os.path.join(ROOT, "tests", "golden", "table2_dirichlet_clamped.txt")):
     line = line.split("#", 1)[0].split()
     if line:
         for j, v in enumerate(line[1:6]):
             if v != "---":
                 TABLE2D[(int(line[0]), 3 + j)] = float(v)
+        for j, v in enumerate(line[6:11]):
+            if v != "---":
+                TABLE2C[(int(line[0]), 3 + j)] = float(v)
 
 
 def main():
@@ -42,19 +45,20 @@ def main():
     ap.add_argument("--fp64", action="store_true")
     ap.add_argument("--forward-post", action="store_true", help="post-smoothing in forward colour order")
     ap.add_argument("--penalty", type=float, default=1.0, help="penalty_scale (reading A2 probe)")
-    ap.add_argument("--kernel", choices=["full", "dirichlet"], default="full")
+    ap.add_argument("--kernel", choices=["full", "dirichlet", "clamped"], default="full")
     a = ap.parse_args()
     for L in [int(v) for v in a.levels.split(",")]:
         for k in [int(v) for v in a.degrees.split(",")]:
             h = ipmg.Handle(3, k, L, vcycle_precision=ipmg.FP64 if a.fp64 else ipmg.FP32,
                             post_smooth_reverse=0 if a.forward_post else 1, penalty_scale=a.penalty,
-                            kernel=ipmg.KERNEL_DIRICHLET if a.kernel == "dirichlet" else ipmg.KERNEL_FULL)
+                            kernel={"full": ipmg.KERNEL_FULL, "dirichlet": ipmg.KERNEL_DIRICHLET,
+                                    "clamped": ipmg.KERNEL_CLAMPED}[a.kernel])
             n = h.ndofs(L - 1)
             b = torch.empty(n, dtype=torch.float64, device="cuda")
             h.rhs(L - 1, b)
             x = torch.empty_like(b)
             r = h.gmres_solve(b, x, rtol=1e-8, max_it=100)
-            paper = TABLE1.get((L, k)) if a.kernel == "full" else TABLE2D.get((L, k))
+            paper = {"full": TABLE1, "dirichlet": TABLE2D, "clamped": TABLE2C}[a.kernel].get((L, k))
             print(json.dumps({"L": L, "k": k, "dofs": n, "nu": r["nu"], "paper": paper, "kernel": a.kernel,
                               "iterations": r["iterations"], "converged": r["converged"],
                               "vcycle": "fp64" if a.fp64 else "fp32", "post": "forward" if a.forward_post else "reverse",
