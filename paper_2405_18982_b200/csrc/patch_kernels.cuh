@@ -827,9 +827,18 @@ __device__ __forceinline__ void stage_neighbors(T* NB, const T* __restrict__ x, 
 // S_b^T M (b already in eigen-space), b > a -> M; operator: b < a -> M (the
 // mass the earlier pass applied to the volume term), b > a -> none.
 // 0 none, 1 mass, 2 S^T M
+#ifndef IPMG_SMOOTHER_EIGEN_FACES
+#define IPMG_SMOOTHER_EIGEN_FACES 0
+#endif
 template <bool SMOOTHER>
 __host__ __device__ constexpr int face_mode(int a, int b) {
+#if IPMG_SMOOTHER_EIGEN_FACES
   return SMOOTHER ? (b < a ? 2 : 1) : (b < a ? 1 : 0);
+#else
+  // smoother: every face family is kept in physical space (tangential cell masses
+  // only) and injected into the right-hand side in the first pass
+  return SMOOTHER ? 1 : (b < a ? 1 : 0);
+#endif
 }
 __host__ __device__ constexpr int first_tan(int a) { return a == 0 ? 1 : 0; }
 __host__ __device__ constexpr int second_tan(int a) { return a == 2 ? 1 : 2; }
@@ -955,7 +964,7 @@ template <int D, bool SMOOTHER, typename T>
 __device__ __forceinline__ void face_transform(T* F, const PInfo<D>* pis, int npc) {
   using C = Cfg<D, T>;
   // first tangential direction: only the S^T M transforms are left (mass was fused)
-  constexpr bool any1 = SMOOTHER;   // families a >= 1 have first tangential b = 0 < a
+  constexpr bool any1 = SMOOTHER && IPMG_SMOOTHER_EIGEN_FACES;   // S^T M transforms along the first tangential
   if (any1) {
     const int nl = (D == 2) ? 1 : NP;             // lines per array
 #pragma unroll 1
@@ -1019,6 +1028,38 @@ __device__ __forceinline__ void face_inject(T (&y)[R][NP], const T* F, int p, in
       T hi = tb.CF[2][NC + i] * uh;
       if (i == NC - 1) hi = fma_(tb.CF[3][NC + i], dh, hi);
       y[r][NC + i] = fma_(sg, hi, y[r][NC + i]);
+    }
+  }
+}
+
+// Smoother: coupling of the face families a >= 1 subtracted from the right-hand
+// side rows of the first (x) pass, in physical space: row (i1[, i2]) gets
+// - sum_{side,kind} CF_{side,kind}(i_a) F_{a,side,kind}[x-index j, other tangential index].
+// Only the side containing i_a contributes (CF_u is zero on the other cell), and
+// the u' kind only on the outermost row.
+template <int D, int R, typename T>
+__device__ __forceinline__ void face_inject_rows(T (&y)[R][NP], const T* F, int p, int g) {
+  using C = Cfg<D, T>;
+  const TabData<K, T>& tb = tab<T>();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int l = g + r * C::G;
+    const int i1 = (D == 2) ? l : l % NP, i2 = (D == 3) ? l / NP : 0;
+#pragma unroll
+    for (int a = 1; a < D; ++a) {
+      const int ia = a == 1 ? i1 : i2;
+      const int s = ia < NC ? 0 : 1;
+      const T cu = tb.CF[2 * s][ia], cd = tb.CF[2 * s + 1][ia];
+      const int other = (D == 3) ? (a == 1 ? i2 : i1) : 0;       // second tangential index
+      const T* fu = F + fofs<D, T>(p, a, s, 0) + other * C::FROW;
+      const T* fd = F + fofs<D, T>(p, a, s, 1) + other * C::FROW;
+      if (cd != T(0)) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) y[r][j] = fma_(-cd, fd[j], fma_(-cu, fu[j], y[r][j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) y[r][j] = fma_(-cu, fu[j], y[r][j]);
+      }
     }
   }
 }
@@ -1259,6 +1300,7 @@ __device__ void fd_pre(T (&xr)[Cfg<D, T>::R][NP], T* X, const T* F, const PInfo<
   for_groups<D, T>(0, npc, [&](int p, int g, int base, int gap, int stride) {
     T w[R][NP];
     if (FACES) face_inject<D, -1, R>(xr, F, p, 0, g);
+    if (FACES && !IPMG_SMOOTHER_EIGEN_FACES) face_inject_rows<D, R>(xr, F, p, g);
     fwd_line<R>(xr, w, pis[p].var[0]);
     store_lines<NP, R>(X + base, gap, stride, w);
   });
@@ -1267,7 +1309,7 @@ __device__ void fd_pre(T (&xr)[Cfg<D, T>::R][NP], T* X, const T* F, const PInfo<
     for_groups<D, T>(1, npc, [&](int p, int g, int base, int gap, int stride) {
       T v[R][NP], w[R][NP];
       load_lines<NP, R>(X + base, gap, stride, v);
-      if (FACES) face_inject<D, -1, R>(v, F, p, 1, g);
+      if (FACES && IPMG_SMOOTHER_EIGEN_FACES) face_inject<D, -1, R>(v, F, p, 1, g);
       fwd_line<R>(v, w, pis[p].var[1]);
       store_lines<NP, R>(X + base, gap, stride, w);
     });
@@ -1298,7 +1340,7 @@ __device__ void fd_post(T* X, const T* F, const PInfo<D>* pis, int npc, Out&& ou
     }
     T v[R][NP], w[R][NP];
     load_lines<NP, R>(X + base, gap, stride, v);
-    if (FACES) face_inject<D, -1, R>(v, F, p, LAST, g);
+    if (FACES && IPMG_SMOOTHER_EIGEN_FACES) face_inject<D, -1, R>(v, F, p, LAST, g);
     IPMG_VAR_SPLIT(pi.var[LAST], (fd_last<0, R>(v, w, lsum, lact)), (fd_last_rt<R>(v, w, lsum, lact, v_)));
     store_lines<NP, R>(X + base, gap, stride, v);
   });
