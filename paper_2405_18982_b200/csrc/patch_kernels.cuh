@@ -1363,6 +1363,103 @@ __device__ void fd_post(T* X, const T* F, const PInfo<D>* pis, int npc, Out&& ou
 }
 
 // ---------------------------------------------------------------- kernels
+// ---- b staged by TMA bulk copies (IPMG_TMA_B): one elected thread arms an
+// mbarrier with the byte count and issues one cp.async.bulk per patch cell right
+// after the setup, so the HBM reads of b overlap the face-trace phase without
+// holding registers; the first pass then reads its rows from shared memory.
+#ifndef IPMG_TMA_B
+#define IPMG_TMA_B 0   // measured: slower (2D k=7 colour pass 0.265 -> 0.329 ms), see DESIGN.md 4.7
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(smem_u32(m)), "r"(phase)
+                 : "memory");
+}
+template <int D, typename T>
+struct Stage {
+  using C = Cfg<D, T>;
+  static constexpr bool ALIGNED = (C::CELL * (int)sizeof(T)) % 16 == 0;      // every cell 16-byte aligned
+  static constexpr int SPB = ALIGNED ? C::CELL : ((C::CELL * (int)sizeof(T) + 31) / 16 + 1) * 16 / (int)sizeof(T);
+  static constexpr int ELEMS = C::PPC * C::NCH * SPB;                        // staging elements per CTA
+};
+// thread 0: arm the barrier and copy the patch cells of src (valid patches) into BS;
+// boff[p*NCH+q]: element offset of the cell inside its slot (16-byte widening)
+template <int D, typename T>
+__device__ __forceinline__ void stage_cells(T* BS, int* boff, const T* __restrict__ src, const PInfo<D>* pis,
+                                            unsigned long long* mbar) {
+  using C = Cfg<D, T>;
+  using St = Stage<D, T>;
+  if (threadIdx.x != 0) return;
+  unsigned total = 0;
+  for (int p = 0; p < C::PPC; ++p)
+    if (pis[p].valid)
+      for (int q = 0; q < C::NCH; ++q) {
+        const unsigned long long a = (unsigned long long)(src + pis[p].coff[q]);
+        const unsigned long long a0 = a & ~15ull, a1 = (a + C::CELL * sizeof(T) + 15) & ~15ull;
+        total += (unsigned)(a1 - a0);
+      }
+  mbar_expect_tx(mbar, total);
+  for (int p = 0; p < C::PPC; ++p) {
+    if (!pis[p].valid) continue;
+    for (int q = 0; q < C::NCH; ++q) {
+      const unsigned long long a = (unsigned long long)(src + pis[p].coff[q]);
+      const unsigned long long a0 = a & ~15ull, a1 = (a + C::CELL * sizeof(T) + 15) & ~15ull;
+      boff[p * C::NCH + q] = (int)((a - a0) / sizeof(T));
+      bulk_g2s(BS + (p * C::NCH + q) * St::SPB, (const void*)a0, (unsigned)(a1 - a0), mbar);
+    }
+  }
+}
+// rows of this thread's x-pass line group from the staged cells
+template <int D, typename T>
+__device__ __forceinline__ void my_rows_staged(const T* BS, const int* boff, const PInfo<D>* pis, int npc, T scale,
+                                               T (&v)[Cfg<D, T>::R][NP]) {
+  using C = Cfg<D, T>;
+  using St = Stage<D, T>;
+  const int u = threadIdx.x;
+  if (u >= npc * C::G) return;
+  const int p = u / C::G, g = u % C::G;
+#pragma unroll
+  for (int r = 0; r < C::R; ++r) {
+    if (!pis[p].valid) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) v[r][j] = T(0);
+      continue;
+    }
+    int qlo, r0;
+    row_cells<D>(g + r * C::G, qlo, r0);
+    const T* s0 = BS + (p * C::NCH + qlo) * St::SPB + r0 + (St::ALIGNED ? 0 : boff[p * C::NCH + qlo]);
+    const T* s1 = BS + (p * C::NCH + qlo + 1) * St::SPB + r0 + (St::ALIGNED ? 0 : boff[p * C::NCH + qlo + 1]);
+    constexpr int V = St::ALIGNED ? row_vec<T>() : 1;
+    using VT = typename VecT<T, V>::type;
+#pragma unroll
+    for (int c = 0; c < NC / V; ++c) {
+      const VT a = reinterpret_cast<const VT*>(s0)[c], b = reinterpret_cast<const VT*>(s1)[c];
+#pragma unroll
+      for (int w = 0; w < V; ++w) {
+        v[r][c * V + w] = scale * vget<VT, T>(a, w);
+        v[r][NC + c * V + w] = scale * vget<VT, T>(b, w);
+      }
+    }
+  }
+}
+
 // rows of this thread's line group (x-pass) loaded from global into registers
 template <int D, typename T>
 __device__ __forceinline__ void my_rows(const T* __restrict__ src, const PInfo<D>* pis, int npc, T scale,
@@ -1484,10 +1581,29 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_SMOOTH)
   T* F = X + C::PPC * C::TSZ;
   T* NB = F + C::PPC * C::FSZ;   // neighbour staging (C::STAGE)
   __shared__ PInfo<D> pis[C::PPC];
+#if IPMG_TMA_B
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ int boff[C::PPC * C::NCH];
+  T* BS = reinterpret_cast<T*>((reinterpret_cast<unsigned long long>(NB + (C::STAGE ? C::NBS : 0)) + 15) & ~15ull);
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
+#endif
   setup_patches<D, T>(pis, g, colour);
+#if IPMG_TMA_B
+  stage_cells<D, T>(BS, boff, b, pis, &mbar);
+#else
   prefetch_cells<D>(b, pis, C::PPC);
+#endif
   if (x_in != nullptr && C::STAGE) stage_neighbors<D>(NB, x_in, pis, C::PPC);   // lands during fd_pre
   T br[C::R][NP];
+#if IPMG_TMA_B
+#define IPMG_MY_B_ROWS()                                  \
+  do {                                                    \
+    mbar_wait(&mbar, 0);                                  \
+    my_rows_staged<D>(BS, boff, pis, C::PPC, T(g.hinv), br); \
+  } while (0)
+#else
+#define IPMG_MY_B_ROWS() my_rows<D>(b, pis, C::PPC, T(g.hinv), br)
+#endif
 #ifdef IPMG_ROWS_EARLY
   my_rows<D>(b, pis, C::PPC, T(g.hinv), br);    // in flight while the traces load
 #endif
@@ -1497,17 +1613,18 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_SMOOTH)
   if (x_in != nullptr) {
     faces_prepare<D, true>(F, x_in, NB, pis, C::PPC);
 #ifndef IPMG_ROWS_EARLY   // measured: loading the rows after the traces keeps registers low
-    my_rows<D>(b, pis, C::PPC, T(g.hinv), br);
+    IPMG_MY_B_ROWS();
 #endif
     fd_pre<D, true>(br, X, F, pis, C::PPC);
     fd_post<D, true>(X, F, pis, C::PPC, out);
   } else {
 #ifndef IPMG_ROWS_EARLY
-    my_rows<D>(b, pis, C::PPC, T(g.hinv), br);
+    IPMG_MY_B_ROWS();
 #endif
     fd_pre<D, false>(br, X, F, pis, C::PPC);
     fd_post<D, false>(X, F, pis, C::PPC, out);
   }
+#undef IPMG_MY_B_ROWS
 }
 
 // additive Schwarz over one colour: x_j += omega A_jj^{-1} r_j
@@ -1722,8 +1839,9 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
   using C = Cfg<D, T>;
   const dim3 grid = patch_grid<D, T>(g, colour);
   // no neighbour staging (and less shared memory, more CTAs) when x_in == 0
-  const size_t sm = xi ? smem_bytes<D, T>(1, true) : smem_bytes<D, T>(1, false) + sizeof(T) * C::PPC * C::FSZ;
-  cudaError_t e = set_smem(smooth_kernel<D, T>, smem_bytes<D, T>(1, true));
+  const size_t stg = IPMG_TMA_B ? sizeof(T) * (size_t)Stage<D, T>::ELEMS + 16 : 0;   // + alignment slack
+  const size_t sm = (xi ? smem_bytes<D, T>(1, true) : smem_bytes<D, T>(1, false) + sizeof(T) * C::PPC * C::FSZ) + stg;
+  cudaError_t e = set_smem(smooth_kernel<D, T>, smem_bytes<D, T>(1, true) + stg);
   if (e != cudaSuccess) return e;
   if (grid.x * grid.y * grid.z > 0) {
     // shifted colours: one extra column of CTAs copies the uncovered boundary layers
