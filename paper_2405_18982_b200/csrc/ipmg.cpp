@@ -843,6 +843,12 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     st = h->cuda((call), what);                        \
     if (st != IPMG_OK) return st;                      \
   } while (0)
+  // the bandwidth-heavy vector kernels, timed as class KC_BLAS by ipmg_profile
+#define TK(call, bytes, what)                                                         \
+  do {                                                                              \
+    st = h->run(KC_BLAS, L, (double)(bytes), 0, [&] { return (call); }, what);      \
+    if (st != IPMG_OK) return st;                                                   \
+  } while (0)
   std::vector<double> hist;
   // slots: 0/1 rz (alternating), 2 pq, 3 rr
   CK(cudaMemsetAsync(x, 0, n * 8, s), "memset x");
@@ -875,10 +881,10 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       st = h->vcycle_level(L, IPMG_FP32);
       if (st != IPMG_OK) return st;
       h->n_launches += 3;
-      CK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), "dot");
+      TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
       CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
       if ((st = h->allsum(h->scal + cur)) != IPMG_OK) return st;
-      CK(ipmg::cg_update_p32(h->p, z32, n, h->scal, cur, -1, s), "p = z");
+      TK(ipmg::cg_update_p32(h->p, z32, n, h->scal, cur, -1, s), 12.0 * n, "p = z");
     } else {
       st = h->vcycle(h->r, h->z, h->partial);
       if (st != IPMG_OK) return st;
@@ -897,7 +903,8 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       h->n_launches += 3;
       CK(ipmg::finalize(h->partial, h->scal + 2, s, nparts), "finalize");
       if ((st = h->allsum(h->scal + 2)) != IPMG_OK) return st;
-      CK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s, r32), "update");
+      TK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s, r32),
+         (48.0 + (r32 ? 4.0 : 0.0)) * n, "update");
       CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
       if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
       CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
@@ -910,10 +917,10 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
         st = h->vcycle_level(L, IPMG_FP32);
         if (st != IPMG_OK) return st;
         h->n_launches += 3;
-        CK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), "dot");
+        TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
         CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
         if ((st = h->allsum(h->scal + (1 - cur))) != IPMG_OK) return st;
-        CK(ipmg::cg_update_p32(h->p, z32, n, h->scal, 1 - cur, cur, s), "update p");
+        TK(ipmg::cg_update_p32(h->p, z32, n, h->scal, 1 - cur, cur, s), 20.0 * n, "update p");
       } else {
         st = h->vcycle(h->r, h->z, h->partial);
         if (st != IPMG_OK) return st;
@@ -926,6 +933,7 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     }
   }
 #undef CK
+#undef TK
   auto t1 = std::chrono::steady_clock::now();
   if (info) {
     info->iterations = it;
