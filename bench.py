@@ -219,8 +219,10 @@ def run_ours(args, rank, ws, local):
         import torch.distributed as dist
     wl = WORKLOAD
     comm = ipmg.Comm.from_torch_distributed(local) if ws > 1 else None
+    # multi-GPU: levels where a rank would keep < 1M dofs are replicated (their halo
+    # exchanges would cost more NCCL latency than computing them redundantly)
     h = ipmg.Handle(wl["dim"], wl["degree"], wl["n_levels"], coarse_cells=wl["coarse"],
-                    vcycle_precision=ipmg.FP32, device=local, comm=comm)
+                    vcycle_precision=ipmg.FP32, device=local, comm=comm, dist_min_dofs=1 << 20)
     L = wl["n_levels"] - 1
     n = h.ndofs(L)                      # this rank's dofs (slab of the finest level)
     n_glob = n

@@ -97,6 +97,8 @@ typedef struct {
   void *cuda_stream;        /* cudaStream_t all work is enqueued on                        */
   ipmg_comm *comm;          /* NULL: one GPU; else this rank's communicator (not owned)    */
   int basis;                /* ipmg_basis; CLAMPED needs HERMITE, DIRICHLET needs LAGRANGE */
+  int64_t dist_min_dofs;    /* with a communicator: distribute a level only if every rank keeps
+                               >= this many of its dofs (else replicate it); 0: whenever possible */
 } ipmg_config;
 
 typedef struct ipmg_handle ipmg_handle;
@@ -140,9 +142,10 @@ ipmg_status ipmg_level_partition(const ipmg_handle *h, int level, int *distribut
  * of `nranks`.  Rule: level l >= 1 is distributed iff its global layer count
  * along the slowest axis is a multiple of 2*nranks (every rank owns an even
  * number >= 2 of layers, so colour-0 patches and parent cells never straddle
- * ranks); with nranks = 1 every level is "distributed" (zoff 0). */
+ * ranks) and every rank keeps >= min_local_dofs of its dofs (degree k sets the
+ * dofs per cell); with nranks = 1 every level is "distributed" (zoff 0). */
 ipmg_status ipmg_partition(int dim, const int coarse_cells[3], int n_levels, int nranks, int rank,
-                           int level, int out[4]);
+                           int level, int degree, int64_t min_local_dofs, int out[4]);
 
 /* Communicators.  ipmg_nccl_unique_id writes 128 bytes (host) that rank 0
  * broadcasts (e.g. through torch.distributed) to every rank, which then calls

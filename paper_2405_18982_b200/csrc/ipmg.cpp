@@ -38,10 +38,18 @@ namespace {
 std::string g_create_error;
 
 // partition rule of the slab decomposition (ipmg.h ipmg_partition)
-void partition_rule(int dim, const int cc[3], int l, int nranks, int rank, int out[4]) {
+// min_local_dofs: a level is only distributed if every rank keeps at least this
+// many dofs of it (coarser levels are replicated: their halo exchanges would cost
+// more latency than computing them redundantly); 0 = distribute whenever possible
+void partition_rule(int dim, const int cc[3], int l, int nranks, int rank, int out[4], int degree = 1,
+                    long long min_local_dofs = 0) {
   const int S = dim - 1;
   const long long ng = (long long)cc[S] << l;
-  const int dist = nranks == 1 ? 1 : (l >= 1 && ng % (2LL * nranks) == 0 ? 1 : 0);
+  long long layer_dofs = 1;
+  for (int a = 0; a < dim - 1; ++a) layer_dofs *= (long long)cc[a] << l;
+  for (int a = 0; a < dim; ++a) layer_dofs *= degree + 1;
+  const bool big = ng / (nranks > 0 ? nranks : 1) * layer_dofs >= min_local_dofs;
+  const int dist = nranks == 1 ? 1 : (l >= 1 && ng % (2LL * nranks) == 0 && big ? 1 : 0);
   out[0] = dist;
   out[3] = (int)ng;
   out[2] = dist ? (int)(ng / nranks) : (int)ng;
@@ -403,6 +411,7 @@ void ipmg_config_default(ipmg_config* c) {
   c->vcycle_precision = IPMG_FP32;
   c->penalty_scale = 1.0;
   c->basis = IPMG_BASIS_LAGRANGE;
+  c->dist_min_dofs = 0;
   c->device = 0;
   c->cuda_stream = nullptr;
 }
@@ -522,7 +531,7 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
     g.n[2] = 1;
     for (int a = 0; a < h->dim; ++a) g.n[a] = cfg->coarse_cells[a] << l;
     int part[4];
-    partition_rule(h->dim, cfg->coarse_cells, l, h->nranks, h->rank, part);
+    partition_rule(h->dim, cfg->coarse_cells, l, h->nranks, h->rank, part, h->k, cfg->dist_min_dofs);
     g.n[h->dim - 1] = part[2];
     g.zoff = part[1];
     g.nglob = part[3];
@@ -628,13 +637,14 @@ ipmg_status ipmg_destroy(ipmg_handle* h) {
 }
 
 ipmg_status ipmg_partition(int dim, const int coarse_cells[3], int n_levels, int nranks, int rank, int level,
-                           int out[4]) {
+                           int degree, int64_t min_local_dofs, int out[4]) {
   if ((dim != 2 && dim != 3) || !coarse_cells || !out || n_levels < 1 || level < 0 || level >= n_levels ||
       nranks < 1 || rank < 0 || rank >= nranks)
     return IPMG_ERR_INVALID_ARG;
   for (int a = 0; a < dim; ++a)
     if (coarse_cells[a] != 1 && coarse_cells[a] != 2) return IPMG_ERR_INVALID_ARG;
-  partition_rule(dim, coarse_cells, level, nranks, rank, out);
+  if (degree < 1 || degree > 7 || min_local_dofs < 0) return IPMG_ERR_INVALID_ARG;
+  partition_rule(dim, coarse_cells, level, nranks, rank, out, degree, min_local_dofs);
   return IPMG_OK;
 }
 

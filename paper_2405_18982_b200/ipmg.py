@@ -39,7 +39,8 @@ class Config(ctypes.Structure):
                 ("smoother", ctypes.c_int), ("additive_omega", ctypes.c_double),
                 ("post_smooth_reverse", ctypes.c_int), ("vcycle_precision", ctypes.c_int),
                 ("penalty_scale", ctypes.c_double), ("device", ctypes.c_int),
-                ("cuda_stream", ctypes.c_void_p), ("comm", ctypes.c_void_p), ("basis", ctypes.c_int)]
+                ("cuda_stream", ctypes.c_void_p), ("comm", ctypes.c_void_p), ("basis", ctypes.c_int),
+                ("dist_min_dofs", ctypes.c_int64)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -87,7 +88,7 @@ def load():
         "ipmg_launch_count": (i, [vp, ctypes.POINTER(ctypes.c_int64)]),
         "ipmg_level_partition": (i, [vp, i, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                      ctypes.POINTER(ctypes.c_int)]),
-        "ipmg_partition": (i, [i, ctypes.c_int * 3, i, i, i, i, ctypes.c_int * 4]),
+        "ipmg_partition": (i, [i, ctypes.c_int * 3, i, i, i, i, i, ctypes.c_int64, ctypes.c_int * 4]),
         "ipmg_nccl_unique_id": (i, [ctypes.c_char_p]),
         "ipmg_comm_create_nccl": (i, [ctypes.c_char_p, i, i, i, ctypes.POINTER(vp)]),
         "ipmg_comm_create_local": (i, [i, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)]),
@@ -118,12 +119,12 @@ def tables_1d(k, what, penalty_scale=1.0):
     return np.array(buf[:n.value])
 
 
-def partition(dim, coarse_cells, n_levels, nranks, rank, level):
+def partition(dim, coarse_cells, n_levels, nranks, rank, level, degree=1, min_local_dofs=0):
     """Host-only slab partition rule (ipmg_partition): (distributed, zoff, local_layers, global_layers)."""
     lib = load()
     cc = (ctypes.c_int * 3)(*(list(coarse_cells) + [1] * (3 - len(coarse_cells))))
     out = (ctypes.c_int * 4)()
-    st = lib.ipmg_partition(dim, cc, n_levels, nranks, rank, level, out)
+    st = lib.ipmg_partition(dim, cc, n_levels, nranks, rank, level, degree, min_local_dofs, out)
     if st != IPMG_OK:
         raise IpmgError(st, "ipmg_partition")
     return tuple(out)
@@ -192,7 +193,7 @@ class Handle:
 
     def __init__(self, dim, degree, n_levels, coarse_cells=None, h0=0.5, smoother=MULTIPLICATIVE,
                  additive_omega=0.0, post_smooth_reverse=1, vcycle_precision=FP32, penalty_scale=1.0,
-                 device=0, stream=None, comm=None, kernel=KERNEL_FULL, basis=None):
+                 device=0, stream=None, comm=None, kernel=KERNEL_FULL, basis=None, dist_min_dofs=0):
         import torch
         self.lib = load()
         cfg = Config()
@@ -205,6 +206,7 @@ class Handle:
         cfg.post_smooth_reverse, cfg.vcycle_precision = post_smooth_reverse, vcycle_precision
         cfg.penalty_scale, cfg.device = penalty_scale, device
         cfg.kernel = kernel
+        cfg.dist_min_dofs = dist_min_dofs
         # the clamped kernel lives on the Hermite-type basis (the whole hierarchy)
         cfg.basis = (BASIS_HERMITE if kernel == KERNEL_CLAMPED else BASIS_LAGRANGE) if basis is None else basis
         if stream is None:

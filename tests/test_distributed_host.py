@@ -104,3 +104,13 @@ def test_gloo_two_ranks_bootstrap_and_partition():
             assert d0[1] == 0 and d1[1] == d0[2] and d0[2] + d1[2] == d0[3]
         else:
             assert d0 == d1
+
+
+def test_partition_min_local_dofs_replicates_coarse_levels():
+    """C2 (2D k=7, 10 levels) on 8 ranks with a 1M-dof floor: only the levels
+    where every rank keeps >= 2^20 dofs are distributed (9 and 8), a suffix of
+    the hierarchy; without the floor levels 3..9 are."""
+    d0 = [ipmg.partition(2, (2, 2), 10, 8, 0, l, 7, 0)[0] for l in range(10)]
+    d1 = [ipmg.partition(2, (2, 2), 10, 8, 0, l, 7, 1 << 20)[0] for l in range(10)]
+    assert d0 == [0, 0, 0, 1, 1, 1, 1, 1, 1, 1]
+    assert d1 == [0, 0, 0, 0, 0, 0, 0, 0, 1, 1]

@@ -302,3 +302,32 @@ def test_dirichlet_smoother_bit_identical():
             assert torch.equal(t.join(level, xs), xser), "level %d" % level
     finally:
         t.close()
+
+
+def test_replicated_grouped_levels_bit_identical():
+    """dist_min_dofs replicates the coarse levels early: the distributed ->
+    replicated transition then lands on a parent-grouped level (here 4 -> 2 of a
+    5-level 2D hierarchy); V-cycle bit-identical, CG as the serial solve."""
+    _need_gpu()
+    t = Team(2, 3, 5, 2, None, dist_min_dofs=2000)
+    try:
+        assert [t.h[0].level_partition(l)[0] for l in range(5)] == [0, 0, 0, 1, 1]
+        L = t.nl - 1
+        r = rand(t.serial.ndofs(L), 70)
+        z = torch.empty_like(r)
+        t.serial.vcycle(r, z)
+        rs = t.split(L, r)
+        zs = [torch.empty_like(v) for v in rs]
+        t.run(lambda q, h: h.vcycle(rs[q], zs[q]))
+        assert torch.equal(t.join(L, zs), z)
+        b = torch.empty(t.serial.ndofs(L), dtype=torch.float64, device="cuda")
+        t.serial.rhs(L, b)
+        x = torch.empty_like(b)
+        res = t.serial.cg_solve(b, x)
+        bs = t.split(L, b)
+        xs = [torch.empty_like(v) for v in bs]
+        out = t.run(lambda q, h: h.cg_solve(bs[q], xs[q]))
+        assert all(o["iterations"] == res["iterations"] for o in out)
+        assert float(torch.linalg.norm(t.join(L, xs) - x) / torch.linalg.norm(x)) <= 1e-12
+    finally:
+        t.close()
