@@ -359,6 +359,18 @@ cudaError_t combine(double* x, const double* const* Z, const double* y, int m, l
   return cudaGetLastError();
 }
 
+// small results to MAPPED pinned host memory by a kernel store (PCIe posted
+// writes): a cudaMemcpy D2H would queue behind bulk copies on the copy engine
+// (e.g. a concurrent download of the previous solution)
+__global__ void to_host_kernel(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+cudaError_t to_host(double* dst_mapped, const double* src, int n, cudaStream_t s) {
+  to_host_kernel<<<1, 64, 0, s>>>(dst_mapped, src, n);
+  return cudaGetLastError();
+}
+
 cudaError_t pattern_fill(double* b, const double* pat, int cell, long long n, cudaStream_t s) {
   pattern_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(b, pat, cell, n);
   return cudaGetLastError();

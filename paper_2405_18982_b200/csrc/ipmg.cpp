@@ -103,6 +103,7 @@ struct ipmg_handle {
   // PCG workspace (finest level, fp64)
   double *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr;
   double *partial = nullptr, *scal = nullptr, *hpin = nullptr, *pattern = nullptr;
+  double *hpin_dev = nullptr, *ghpin_dev = nullptr;   // device aliases of the mapped pinned buffers
   long long partial_len = 0;
   std::vector<void*> allocs;
   std::string err;
@@ -614,7 +615,11 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
       return bail(IPMG_ERR_CUDA);
     }
   }
-  if (cudaMallocHost(&h->hpin, sizeof(double) * 8) != cudaSuccess) { h->err = "pinned alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
+  if (cudaHostAlloc(&h->hpin, sizeof(double) * 8, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&h->hpin_dev, h->hpin, 0) != cudaSuccess) {
+    h->err = "mapped pinned alloc";
+    return bail(IPMG_ERR_OUT_OF_MEMORY);
+  }
   ipmg_status st = h->ensure_vcycle(h->cfg.vcycle_precision);
   if (st != IPMG_OK) return bail(st);
   *out = h;
@@ -867,7 +872,8 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
   CK(ipmg::dot_partial(0, 0, h->r, h->r, n, h->partial, s), "dot");
   CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
   if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
-  CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
+  h->n_launches += 1;
   CK(cudaStreamSynchronize(s), "sync");
   const double r0 = std::sqrt(h->hpin[0]);
   hist.push_back(r0);
@@ -917,7 +923,8 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
          (48.0 + (r32 ? 4.0 : 0.0)) * n, "update");
       CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
       if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
-      CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
+      CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
+  h->n_launches += 1;
       CK(cudaStreamSynchronize(s), "sync");
       ++it;
       const double rn = std::sqrt(h->hpin[0]);
@@ -987,7 +994,9 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
     h->gzptr = (const double**)h->dalloc(sizeof(double*) * (max_it + 1));
     if (h->ghpin) cudaFreeHost(h->ghpin);
     h->ghpin = nullptr;
-    if (!h->ghcol || !h->gy || !h->gzptr || cudaMallocHost(&h->ghpin, sizeof(double) * (max_it + 2)) != cudaSuccess)
+    if (!h->ghcol || !h->gy || !h->gzptr ||
+        cudaHostAlloc(&h->ghpin, sizeof(double) * (max_it + 2), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&h->ghpin_dev, h->ghpin, 0) != cudaSuccess)
       return h->fail(IPMG_ERR_OUT_OF_MEMORY, "GMRES workspace");
     h->gcap = max_it;
   }
@@ -1005,7 +1014,8 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
   CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
   h->n_launches += 2;
   if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
-  CK(cudaMemcpyAsync(h->hpin, h->scal + 3, 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
+  h->n_launches += 1;
   CK(cudaStreamSynchronize(s), "sync");
   const double beta0 = std::sqrt(h->hpin[0]);
   hist.push_back(beta0);
@@ -1058,7 +1068,8 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
       // v_{j+1} = w / ||w|| (and its fp32 copy as the next V-cycle input)
       CK(ipmg::scale_vec(vn, h->gw, n, h->ghcol + j + 1, 0.0, r32, s), "scale");
       h->n_launches += 1;
-      CK(cudaMemcpyAsync(h->ghpin, h->ghcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, s), "d2h");
+      CK(ipmg::to_host(h->ghpin_dev, h->ghcol, j + 2, s), "to host");
+      h->n_launches += 1;
       CK(cudaStreamSynchronize(s), "sync");
       for (int i = 0; i <= j; ++i) Hij(i, j) = h->ghpin[i];
       Hij(j + 1, j) = std::sqrt(h->ghpin[j + 1]);
