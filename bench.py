@@ -199,7 +199,7 @@ def run_reference(args, rank, ws):
     value = n / sec / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp32 V-cycle)", "data": "synthetic (f=1)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 V-cycle)", "data": "synthetic (f=1)",
             "config": {"workload": WORKLOAD["name"] + ": " + WORKLOAD["desc"], "sample": sample_desc()},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample_desc()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

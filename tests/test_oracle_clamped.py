@@ -53,7 +53,7 @@ def _T(dim, k, ncells):
     Tc = np.ones((1, 1))
     for _ in range(dim):
         Tc = np.kron(T1, Tc)
-    return sp.block_diag([Tc] * ncells).tocsr()
+    return sp.kron(sp.identity(ncells, format="csr"), sp.csr_matrix(Tc), format="csr")
 
 
 @pytest.mark.parametrize("dim,k", [(2, 3), (2, 5), (3, 3)])
