@@ -32,6 +32,11 @@ struct LevelGeom {
   double hinv;         // h^(2-d)
   int zoff;            // global index of local cell 0 along the slowest axis
   int nglob;           // global cells along the slowest axis
+  // patch-block selection along the slowest axis (halo/compute overlap): 0 all,
+  // 1 interior blocks (no ghost access), 2 the first and last block; znb = the
+  // launch's full block count along that axis (set by the launchers)
+  int zsel;
+  int znb;
 };
 
 // "no neighbour" marker of patch neighbour offsets (ghost offsets are negative)

@@ -113,6 +113,11 @@ struct ipmg_handle {
   std::vector<int> dist;              // level distributed over the ranks (1) or replicated (0)
   std::vector<long long> ghost;       // elements of one ghost parent layer (0: no ghosts)
   double* gbuf = nullptr;             // allgathered per-rank scalars
+  // halo/compute overlap: the exchange runs on cstream while the interior patch
+  // blocks (which never touch ghosts) run on the main stream
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool overlap = true;
   std::vector<void*> gsc[2][3];       // ghosted copies of caller vectors (API calls), [prec][slot][level]
   // ---- the finest-level V-cycle captured as a CUDA graph per precision
   // ---- GMRES workspace (finest level, fp64): Krylov basis V, preconditioned Z
@@ -199,6 +204,39 @@ struct ipmg_handle {
     if (!comm->halo(xb, xb + nb - gb, xb - gb, xb + nb, gb, stream)) return fail(IPMG_ERR_NCCL, comm->err);
     return IPMG_OK;
   }
+  // halo exchange of x followed by a patch kernel that reads x's ghosts:
+  // kernel(g) launches with the level geometry g; with several ranks the halo is
+  // forked onto cstream, the interior blocks (zsel 1) run meanwhile, and the first
+  // and last blocks (zsel 2) after the join.  bytes: algorithmic bytes (profiling).
+  template <class K>
+  ipmg_status halo_then(int level, int prec, const void* x, int cls, double bytes, K&& kernel, const char* what) {
+    if (!comm || ghost[level] == 0)
+      return run(cls, level, bytes, 1, [&] { return kernel(geom[level]); }, what);
+    if (!overlap || !cstream) {
+      ipmg_status st = halo(level, prec, x);
+      if (st != IPMG_OK) return st;
+      return run(cls, level, bytes, 1, [&] { return kernel(geom[level]); }, what);
+    }
+    ipmg::LevelGeom gi = geom[level], gb = geom[level];
+    gi.zsel = 1;
+    gb.zsel = 2;
+    ipmg_status st = cuda(cudaEventRecord(ev_fork, stream), "fork");
+    if (st != IPMG_OK) return st;
+    st = cuda(cudaStreamWaitEvent(cstream, ev_fork, 0), "fork");
+    if (st != IPMG_OK) return st;
+    {
+      const size_t es = esize(prec), gbs = (size_t)ghost[level] * es, nb = (size_t)ndofs[level] * es;
+      char* xb = (char*)const_cast<void*>(x);
+      if (!comm->halo(xb, xb + nb - gbs, xb - gbs, xb + nb, gbs, cstream)) return fail(IPMG_ERR_NCCL, comm->err);
+    }
+    st = cuda(cudaEventRecord(ev_join, cstream), "join");
+    if (st != IPMG_OK) return st;
+    st = run(cls, level, 0.0, 1, [&] { return kernel(gi); }, what);   // bytes booked on the second launch
+    if (st != IPMG_OK) return st;
+    st = cuda(cudaStreamWaitEvent(stream, ev_join, 0), "join");
+    if (st != IPMG_OK) return st;
+    return run(cls, level, bytes, 1, [&] { return kernel(gb); }, what);
+  }
   // device scalar -> its sum over the ranks (rank order, identical everywhere)
   ipmg_status allsum(double* slot) {
     if (!comm || nranks == 1) return IPMG_OK;
@@ -245,6 +283,14 @@ struct ipmg_handle {
                },
                "smooth_colour");
   }
+  // colour pass whose x_in ghosts come from the neighbour ranks (halo overlapped)
+  ipmg_status smooth_colour_halo(int level, int prec, const void* xi, const void* b, void* xo, int colour) {
+    return halo_then(level, prec, xi, KC_SMOOTH, smooth_bytes(level, prec, colour, true),
+                     [&](const ipmg::LevelGeom& g) {
+                       return (cfg.kernel != IPMG_KERNEL_FULL ? ksd : ks).smooth(dim, prec, xi, b, xo, g, colour, stream);
+                     },
+                     "smooth_colour");
+  }
   // multiplicative step: passes ping-pong between x and other; 2^d passes -> ends in x
   ipmg_status smooth_mult(int level, int prec, void* x, void* other, const void* b, bool reverse, bool x_is_zero) {
     const int ncol = 1 << dim;
@@ -253,11 +299,8 @@ struct ipmg_handle {
     for (int i = 0; i < ncol; ++i) {
       const int c = reverse ? ncol - 1 - i : i;
       const bool zero = i == 0 && x_is_zero;
-      if (!zero) {   // every colour reads face traces of the neighbour slabs
-        ipmg_status st = halo(level, prec, cur);
-        if (st != IPMG_OK) return st;
-      }
-      ipmg_status st = smooth_colour(level, prec, zero ? nullptr : cur, b, nxt, c);
+      // every colour with x reads face traces (and straddling cells) of the neighbour slabs
+      ipmg_status st = zero ? smooth_colour(level, prec, nullptr, b, nxt, c) : smooth_colour_halo(level, prec, cur, b, nxt, c);
       if (st != IPMG_OK) return st;
       std::swap(cur, nxt);
     }
@@ -270,10 +313,9 @@ struct ipmg_handle {
   ipmg_status smooth_add(int level, int prec, void* x, void* rbuf, const void* b, bool x_is_zero) {
     const void* r = b;
     if (!x_is_zero) {
-      ipmg_status st = halo(level, prec, x);
-      if (st != IPMG_OK) return st;
-      st = run(KC_VMULT, level, 3.0 * esize(prec) * ndofs[level], 1,
-               [&] { return ks.vmult(dim, prec, x, rbuf, geom[level], b, nullptr, nullptr, stream); }, "residual");
+      ipmg_status st = halo_then(level, prec, x, KC_VMULT, 3.0 * esize(prec) * ndofs[level],
+                                 [&](const ipmg::LevelGeom& g) { return ks.vmult(dim, prec, x, rbuf, g, b, nullptr, nullptr, stream); },
+                                 "residual");
       if (st != IPMG_OK) return st;
       st = halo(level, prec, rbuf);   // straddling patches read r on the ghost cells
       if (st != IPMG_OK) return st;
@@ -298,14 +340,17 @@ struct ipmg_handle {
   // one V-cycle on level l of the workspace of precision prec: input vb[l],
   // output vx1[l]
   // r_c = P^T (b - A x) (x ghosts current), with the distributed -> replicated transition
-  ipmg_status restrict_to(int l, int prec, const void* x, const void* b, void* rc) {
+  // x_halo: exchange x's ghosts first (overlapped with the interior parents)
+  ipmg_status restrict_to(int l, int prec, const void* x, const void* b, void* rc, bool x_halo = false) {
     ipmg_status st;
     if (transition(l)) {
       st = cuda(cudaMemsetAsync(rc, 0, ndofs[l - 1] * esize(prec), stream), "memset");
       if (st != IPMG_OK) return st;
     }
-    st = run(KC_RESTRICT, l, esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]), 1,
-             [&] { return ks.restrict_(dim, prec, x, b, rc, geom[l], geom[l - 1], stream); }, "restrict");
+    const double by = esize(prec) * (2.0 * ndofs[l] + ndofs[l - 1]);
+    auto kern = [&](const ipmg::LevelGeom& g) { return ks.restrict_(dim, prec, x, b, rc, g, geom[l - 1], stream); };
+    st = (x_halo && x) ? halo_then(l, prec, x, KC_RESTRICT, by, kern, "restrict")
+                       : run(KC_RESTRICT, l, by, 1, [&] { return kern(geom[l]); }, "restrict");
     if (st != IPMG_OK || !transition(l)) return st;
     if (!comm->allreduce_sum(rc, ndofs[l - 1], prec, stream)) return fail(IPMG_ERR_NCCL, comm->err);
     return IPMG_OK;
@@ -323,9 +368,7 @@ struct ipmg_handle {
     else st = smooth_mult(l, prec, x1, x0, b, false, true);
     if (st != IPMG_OK) return st;
     // (2) coarse-grid correction x1 += P P_{l-1}^{-1} P^T (b - A x1)
-    st = halo(l, prec, x1);
-    if (st != IPMG_OK) return st;
-    st = restrict_to(l, prec, x1, b, vb[prec][l - 1]);
+    st = restrict_to(l, prec, x1, b, vb[prec][l - 1], true);
     if (st != IPMG_OK) return st;
     st = l == nlev - 1 ? run_coarse_vcycle(prec) : vcycle_level(l - 1, prec);
     if (st != IPMG_OK) return st;
@@ -597,6 +640,16 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   h->partial = (double*)h->dalloc(sizeof(double) * h->partial_len);
   h->scal = (double*)h->dalloc(sizeof(double) * 8);
   h->gbuf = (double*)h->dalloc(sizeof(double) * 4 * h->nranks);
+  if (h->comm && h->nranks > 1) {
+    const char* no = std::getenv("IPMG_NO_OVERLAP");
+    h->overlap = !(no && no[0] == '1');
+    if (cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      h->err = "comm stream / events";
+      return bail(IPMG_ERR_CUDA);
+    }
+  }
   if (!h->pattern || !h->partial || !h->scal || !h->gbuf) { h->err = "alloc"; return bail(IPMG_ERR_OUT_OF_MEMORY); }
   {
     std::vector<double> pat((size_t)h->cell * h->nlev);
@@ -628,6 +681,9 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
 
 ipmg_status ipmg_destroy(ipmg_handle* h) {
   if (!h) return IPMG_OK;
+  if (h->cstream) cudaStreamDestroy(h->cstream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (int p = 0; p < 2; ++p)
     if (h->vgraph[p]) cudaGraphExecDestroy(h->vgraph[p]);
   for (auto& e : h->ev_pool) {
@@ -911,10 +967,11 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     }
     while (it < max_it) {
       long long nparts = 0;
-      if ((st = h->halo(L, IPMG_FP64, h->p)) != IPMG_OK) return st;
-      st = h->run(KC_VMULT, L, 16.0 * n, 1,
-                  [&] { return h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, h->geom[L], nullptr, h->partial, &nparts, s); },
-                  "vmult");
+      st = h->halo_then(L, IPMG_FP64, h->p, KC_VMULT, 16.0 * n,
+                        [&](const ipmg::LevelGeom& g) {
+                          return h->ks.vmult(h->dim, IPMG_FP64, h->p, h->q, g, nullptr, h->partial, &nparts, s);
+                        },
+                        "vmult");
       if (st != IPMG_OK) return st;
       h->n_launches += 3;
       CK(ipmg::finalize(h->partial, h->scal + 2, s, nparts), "finalize");
@@ -1049,10 +1106,11 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
         if (st != IPMG_OK) return st;
       }
       // w = A z_j
-      if ((st = h->halo(L, IPMG_FP64, zj)) != IPMG_OK) return st;
-      st = h->run(KC_VMULT, L, 16.0 * n, 1,
-                  [&] { return h->ks.vmult(h->dim, IPMG_FP64, zj, h->gw, h->geom[L], nullptr, nullptr, nullptr, s); },
-                  "vmult");
+      st = h->halo_then(L, IPMG_FP64, zj, KC_VMULT, 16.0 * n,
+                        [&](const ipmg::LevelGeom& g) {
+                          return h->ks.vmult(h->dim, IPMG_FP64, zj, h->gw, g, nullptr, nullptr, nullptr, s);
+                        },
+                        "vmult");
       if (st != IPMG_OK) return st;
       // modified Gram-Schmidt: h_ij = w.v_i ; w -= h_ij v_i (each step fused with the next dot)
       CK(ipmg::dot_partial(0, 0, h->gw, h->gV[0], n, h->partial, s), "dot");

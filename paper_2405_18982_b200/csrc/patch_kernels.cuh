@@ -542,6 +542,17 @@ __host__ __device__ inline int slab_first(const LevelGeom& g, int shifted) {
   return shifted ? (g.zoff == 0 ? 1 : -1) : 0;
 }
 
+// patch block along the slowest axis of this CTA under the launch's selection
+template <int D>
+__device__ __forceinline__ int slab_block(const LevelGeom& g) {
+  const int b = D == 3 ? (int)blockIdx.z : (int)blockIdx.y;
+  return g.zsel == 0 ? b : (g.zsel == 1 ? b + 1 : (b == 0 ? 0 : g.znb - 1));
+}
+// block count of a selection out of n blocks along the slowest axis
+__host__ __device__ inline int slab_sel_count(int n, int zsel) {
+  return zsel == 0 ? n : (zsel == 1 ? (n > 2 ? n - 2 : 0) : (n < 2 ? n : 2));
+}
+
 __host__ __device__ inline long long num_patches(const LevelGeom& g, int dim, int colour) {
   long long np = 1;
   for (int a = 0; a < dim - 1; ++a) np *= (g.n[a] / 2 - ((colour >> a) & 1));
@@ -633,7 +644,8 @@ __device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g,
 }
 template <int D, typename T>
 __device__ __forceinline__ void setup_patches(PInfo<D>* pis, const LevelGeom& g, int colour) {
-  setup_patches<D, T>(pis, g, colour, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z);
+  const int bS = slab_block<D>(g);
+  setup_patches<D, T>(pis, g, colour, (int)blockIdx.x, D == 3 ? (int)blockIdx.y : bS, D == 3 ? bS : 0);
 }
 
 // L2 prefetch of the patch cells of src (TMA bulk prefetch, one instruction per
@@ -1513,7 +1525,8 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_VMULT) vmult_ke
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < C::NT / 32; ++w) t += wsum[w];
-      dot_partial[blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z)] = t;
+      const long long bS = slab_block<D>(g);   // full-grid index, also under a split launch
+      dot_partial[blockIdx.x + (long long)gridDim.x * (D == 3 ? blockIdx.y + (long long)gridDim.y * bS : bS)] = t;
     }
   }
 }
@@ -1811,11 +1824,15 @@ inline cudaError_t set_smem(F* f, size_t bytes) {
 
 // grid over the colour's patch lattice: (x-blocks of PPC patches, j1, j2)
 template <int D, typename T>
-inline dim3 patch_grid(const LevelGeom& g, int colour) {
+inline dim3 patch_grid(LevelGeom& g, int colour) {   // also sets g.znb (full count along the slowest axis)
   using C = Cfg<D, T>;
   const int m0 = g.n[0] / 2 - (colour & 1);
-  const int m1 = (D == 3) ? g.n[1] / 2 - ((colour >> 1) & 1) : slab_patches(g, 1, (colour >> 1) & 1);
-  const int m2 = (D == 3) ? slab_patches(g, 2, (colour >> 2) & 1) : 1;
+  int m1 = (D == 3) ? g.n[1] / 2 - ((colour >> 1) & 1) : slab_patches(g, 1, (colour >> 1) & 1);
+  int m2 = (D == 3) ? slab_patches(g, 2, (colour >> 2) & 1) : 1;
+  int& mS = D == 3 ? m2 : m1;
+  mS = mS > 0 ? mS : 0;
+  g.znb = mS;
+  mS = slab_sel_count(mS, g.zsel);
   return dim3((unsigned)((m0 + C::PPC - 1) / C::PPC), (unsigned)(m1 > 0 ? m1 : 0), (unsigned)(m2 > 0 ? m2 : 0));
 }
 
@@ -1823,21 +1840,23 @@ template <int D, typename T>
 cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp, long long* nparts,
                          cudaStream_t s) {
   using C = Cfg<D, T>;
-  const dim3 grid = patch_grid<D, T>(g, 0);
-  if (nparts) *nparts = (long long)grid.x * grid.y * grid.z;
+  LevelGeom gg = g;
+  const dim3 grid = patch_grid<D, T>(gg, 0);
+  if (nparts) *nparts = (long long)grid.x * (D == 3 ? (long long)grid.y * gg.znb : gg.znb);   // full grid
   if (x == nullptr) return cudaSuccess;   // size query
   const size_t sm = smem_bytes<D, T>(2, true);
   cudaError_t e = set_smem(vmult_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
   if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
-  vmult_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (T*)y, (const T*)bm, g, dotp);
+  vmult_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (T*)y, (const T*)bm, gg, dotp);
   return cudaGetLastError();
 }
 
 template <int D, typename T>
 cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
   using C = Cfg<D, T>;
-  const dim3 grid = patch_grid<D, T>(g, colour);
+  LevelGeom gg = g;
+  const dim3 grid = patch_grid<D, T>(gg, colour);
   // no neighbour staging (and less shared memory, more CTAs) when x_in == 0
   const size_t stg = IPMG_TMA_B ? sizeof(T) * (size_t)Stage<D, T>::ELEMS + 16 : 0;   // + alignment slack
   const size_t sm = (xi ? smem_bytes<D, T>(1, true) : smem_bytes<D, T>(1, false) + sizeof(T) * C::PPC * C::FSZ) + stg;
@@ -1845,11 +1864,11 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
   if (e != cudaSuccess) return e;
   if (grid.x * grid.y * grid.z > 0) {
     // shifted colours: one extra column of CTAs copies the uncovered boundary layers
-    const dim3 g2(grid.x + (colour != 0 ? 1 : 0), grid.y, grid.z);
-    smooth_kernel<D, T><<<g2, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour, (int)grid.x);
+    const dim3 g2(grid.x + (colour != 0 && g.zsel != 2 ? 1 : 0), grid.y, grid.z);
+    smooth_kernel<D, T><<<g2, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, gg, colour, (int)grid.x);
     return cudaGetLastError();
   }
-  if (colour != 0) {   // empty patch lattice (tiny level): copy only
+  if (colour != 0 && g.zsel != 2) {   // empty patch lattice (tiny level / no interior blocks): copy only
     long long cells = 0;
     for (int a = 0; a < D; ++a) {
       if (!((colour >> a) & 1)) continue;
@@ -1861,7 +1880,7 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
     long long blocks = (elems + 255) / 256;
     if (blocks > 4 * 148) blocks = 4 * 148;
     if (blocks < 1) blocks = 1;
-    copy_uncovered_kernel<D, T><<<(unsigned)blocks, 256, 0, s>>>((const T*)xi, (T*)xo, g, colour);
+    copy_uncovered_kernel<D, T><<<(unsigned)blocks, 256, 0, s>>>((const T*)xi, (T*)xo, gg, colour);
     e = cudaGetLastError();
   }
   return e;
@@ -1870,12 +1889,13 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
 template <int D, typename T>
 cudaError_t launch_additive(const void* r, void* x, const LevelGeom& g, int colour, double omega, cudaStream_t s) {
   using C = Cfg<D, T>;
-  const dim3 grid = patch_grid<D, T>(g, colour);
+  LevelGeom gg = g;
+  const dim3 grid = patch_grid<D, T>(gg, colour);
   if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   const size_t sm = smem_bytes<D, T>(1, false);
   cudaError_t e = set_smem(additive_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
-  additive_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)r, (T*)x, g, colour, (T)omega);
+  additive_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)r, (T*)x, gg, colour, (T)omega);
   return cudaGetLastError();
 }
 
@@ -1883,24 +1903,26 @@ template <int D, typename T>
 cudaError_t launch_restrict(const void* x, const void* b, void* rc, const LevelGeom& gf, const LevelGeom& gc,
                             cudaStream_t s) {
   using C = Cfg<D, T>;
-  const dim3 grid = patch_grid<D, T>(gf, 0);
+  LevelGeom gg = gf;
+  const dim3 grid = patch_grid<D, T>(gg, 0);
   if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   const size_t sm = smem_bytes<D, T>(2, true);
   cudaError_t e = set_smem(restrict_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
-  restrict_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (const T*)b, (T*)rc, gf, gc);
+  restrict_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)x, (const T*)b, (T*)rc, gg, gc);
   return cudaGetLastError();
 }
 
 template <int D, typename T>
 cudaError_t launch_prolong(const void* ec, void* xf, const LevelGeom& gf, const LevelGeom& gc, cudaStream_t s) {
   using C = Cfg<D, T>;
-  const dim3 grid = patch_grid<D, T>(gf, 0);
+  LevelGeom gg = gf;
+  const dim3 grid = patch_grid<D, T>(gg, 0);
   if (grid.x * grid.y * grid.z == 0) return cudaSuccess;
   const size_t sm = smem_bytes<D, T>(1, false);
   cudaError_t e = set_smem(prolong_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
-  prolong_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)ec, (T*)xf, gf, gc);
+  prolong_kernel<D, T><<<grid, C::NT, sm, s>>>((const T*)ec, (T*)xf, gg, gc);
   return cudaGetLastError();
 }
 
@@ -1979,17 +2001,18 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT)
 template <int D, typename T>
 cudaError_t launch_smooth_dir(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
   using C = Cfg<D, T>;
-  const dim3 grid = patch_grid<D, T>(g, colour);
+  LevelGeom gg = g;
+  const dim3 grid = patch_grid<D, T>(gg, colour);
   const size_t sm = smem_bytes<D, T>(2, false);
   cudaError_t e = set_smem(smooth_dir_kernel<D, T>, sm);
   if (e != cudaSuccess) return e;
   if (grid.x * grid.y * grid.z > 0) {
-    const dim3 g2(grid.x + (colour != 0 ? 1 : 0), grid.y, grid.z);
-    smooth_dir_kernel<D, T><<<g2, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, g, colour, (int)grid.x);
+    const dim3 g2(grid.x + (colour != 0 && g.zsel != 2 ? 1 : 0), grid.y, grid.z);
+    smooth_dir_kernel<D, T><<<g2, C::NT, sm, s>>>((const T*)xi, (const T*)b, (T*)xo, gg, colour, (int)grid.x);
     return cudaGetLastError();
   }
-  if (colour != 0) {
-    copy_uncovered_kernel<D, T><<<4 * 148, 256, 0, s>>>((const T*)xi, (T*)xo, g, colour);
+  if (colour != 0 && g.zsel != 2) {
+    copy_uncovered_kernel<D, T><<<4 * 148, 256, 0, s>>>((const T*)xi, (T*)xo, gg, colour);
     e = cudaGetLastError();
   }
   return e;
