@@ -936,10 +936,133 @@ __device__ __forceinline__ void trace_unit(T* F, const T* __restrict__ x, const 
   }
 }
 
+// Split trace unit (two threads per unit, partner lanes u and u ^ 1): thread
+// `half` loads the neighbour rows rr = half*CH + i (i < CH) only, so each thread
+// keeps half the rows in flight (the unsplit unit holds all NC rows: 128
+// registers in fp64 at k = 7) and the lanes that the unsplit phase leaves idle
+// (2D: 8 units per patch for 16 line groups) share the load latency.  The
+// partial (u, u') vectors are completed with lane shuffles, both partners apply
+// the tangential mass to the full vectors, and each writes its half.
+template <int D, int A, bool SMOOTHER, typename T>
+__device__ __forceinline__ void trace_unit_split(T* F, const T* __restrict__ x, const PInfo<D>& pi, int p, int s,
+                                                 int h, int ic, int half, bool act) {
+  const TabData<K, T>& tb = tab<T>();
+  constexpr int V = row_vec<T>();
+  using VT = typename VecT<T, V>::type;
+  constexpr int CH = (NC + 1) / 2;
+  const int tc = h + ((D == 3 && ic >= NC) ? 2 : 0);
+  const long long nb = act ? pi.nb[2 * A + s][tc] : NO_NB;
+  // A = 0: own entries rr = half*CH + i in ou/od[i]; A != 0: partial sums over own rows (all lb)
+  T ou[NC], od[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) ou[i] = od[i] = T(0);
+  if (nb != NO_NB) {
+    const int lc = ic % NC;
+    const int off = (D == 3 ? (A == 2 ? NC * lc : NC * NC * lc) : 0);
+    const T* base = x + nb + off;
+    constexpr int RS = (A == 2) ? NC * NC : NC;
+    const int jf = (s == 0) ? NC - 1 : 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int rr = half * CH + i;
+      if (rr >= NC) break;
+      T row[NC];
+#pragma unroll
+      for (int c = 0; c < NC / V; ++c) {
+        const VT val = __ldg(reinterpret_cast<const VT*>(base + rr * RS) + c);
+#pragma unroll
+        for (int v = 0; v < V; ++v) row[c * V + v] = vget<VT, T>(val, v);
+      }
+      if (A == 0) {
+        T acc = T(0);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc = fma_(s == 0 ? tb.d1[j] : tb.d0[j], row[j], acc);
+        od[i] = acc;
+        ou[i] = (s == 0) ? row[NC - 1] : row[0];
+      } else {
+        const T dj = (s == 0) ? tb.d1[rr] : tb.d0[rr];
+#pragma unroll
+        for (int lb = 0; lb < NC; ++lb) od[lb] = fma_(dj, row[lb], od[lb]);
+        if (rr == jf) {
+#pragma unroll
+          for (int lb = 0; lb < NC; ++lb) ou[lb] = row[lb];
+        }
+      }
+    }
+  }
+  // the partner pair only: units of different face families diverge
+  const unsigned pm = 3u << ((threadIdx.x & 31) & ~1u);
+  T u[NC], du[NC];
+  if (A == 0) {   // full vectors: lower half from thread 0, upper from thread 1
+    T pu[CH], pd[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      pu[i] = __shfl_xor_sync(pm, ou[i], 1);
+      pd[i] = __shfl_xor_sync(pm, od[i], 1);
+    }
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      u[i] = half ? pu[i] : ou[i];
+      du[i] = half ? pd[i] : od[i];
+      if (CH + i < NC) {
+        u[CH + i] = half ? ou[i] : pu[i];
+        du[CH + i] = half ? od[i] : pd[i];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      u[i] = ou[i] + __shfl_xor_sync(pm, ou[i], 1);
+      du[i] = od[i] + __shfl_xor_sync(pm, od[i], 1);
+    }
+  }
+  if (face_mode<SMOOTHER>(A, first_tan(A)) == 1) {
+    T in2[2][NC], out2[2][NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      in2[0][i] = u[i];
+      in2[1][i] = du[i];
+    }
+    mv<NC, NC, MassC<T>, 2>(in2, out2, MassC<T>{});
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      u[i] = out2[0][i];
+      du[i] = out2[1][i];
+    }
+  }
+  if (!act) return;
+  T* fu = F + fofs<D, T>(p, A, s, 0);
+  T* fd = F + fofs<D, T>(p, A, s, 1);
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int lb = half * CH + i;
+    if (lb >= NC) break;
+    const int pos = fpos<D, T>(h * NC + lb + NP * ic);
+    fu[pos] = half ? u[CH + i < NC ? CH + i : 0] : u[i];
+    fd[pos] = half ? du[CH + i < NC ? CH + i : 0] : du[i];
+  }
+}
+
 template <int D, bool STAGED, bool SMOOTHER, typename T>
 __device__ __forceinline__ void face_traces(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis, int npc) {
   constexpr int NIC = (D == 3) ? NP : 1;
   constexpr int UPF = 2 * 2 * NIC;                    // units per face family: side x half x ic
+  using C = Cfg<D, T>;
+#ifndef IPMG_TRACE_SPLIT
+#define IPMG_TRACE_SPLIT 2   // 0 never, 1 always (where the pairs fit one pass), 2 fp64 only
+#endif
+  // measured (2D k=7): fp64 operator 0.587 -> 0.497 ms (152 -> 80 registers);
+  // the fp32 smoother colour pass 0.265 -> 0.271 ms, so fp32 keeps one thread per unit
+  if ((IPMG_TRACE_SPLIT == 1 || (IPMG_TRACE_SPLIT == 2 && sizeof(T) == 8)) && !STAGED && 2 * C::PPC * D * UPF <= C::NT) {   // one pass, two threads per unit
+    const int e = threadIdx.x >> 1, half = threadIdx.x & 1;
+    const bool act = e < npc * D * UPF;
+    const int p = act ? e / (D * UPF) : 0, r = e % (D * UPF), a = r / UPF, w = r % UPF;
+    const int s = w & 1, h = (w >> 1) & 1, ic = w >> 2;
+    if (a == 0) trace_unit_split<D, 0, SMOOTHER>(F, x, pis[p], p, s, h, ic, half, act);
+    else if (a == 1) trace_unit_split<D, 1, SMOOTHER>(F, x, pis[p], p, s, h, ic, half, act);
+    else trace_unit_split<D, (D == 3 ? 2 : 1), SMOOTHER>(F, x, pis[p], p, s, h, ic, half, act);
+    return;
+  }
   for (int e = threadIdx.x; e < npc * D * UPF; e += blockDim.x) {
     const int p = e / (D * UPF), r = e % (D * UPF), a = r / UPF, w = r % UPF;
     const int s = w & 1, h = (w >> 1) & 1, ic = w >> 2;
@@ -1250,8 +1373,13 @@ __device__ void vol_last(T* X, T* T1, const T* F, const PInfo<D>* pis, int npc, 
   for_groups<D, T>(LAST, npc, [&](int p, int g, int base, int gap, int stride) {
     T a[R][NP], bb[R][NP], y[R][NP];
     load_lines<NP, R>(X + base, gap, stride, a);
-    load_lines<NP, R>(T1 + base, gap, stride, bb);
     mv<NP, NP, MassP<T>, R>(a, y);
+#if IPMG_VOL_ORDER
+    // a is dead before bb is loaded: two line arrays live instead of three
+    // (fp64 2D k=7 vmult: 152 registers, 18 % occupancy)
+    asm volatile("" ::: "memory");
+#endif
+    load_lines<NP, R>(T1 + base, gap, stride, bb);
     IPMG_VAR_SPLIT(pis[p].var[LAST], (mv_acc<NP, NP, LapP<0, T>, R>(bb, y)),
                    (mv_acc<NP, NP, LapRT<T>, R>(bb, y, LapRT<T>{v_})));
     if (FACES) face_inject<D, 1, R>(y, F, p, LAST, g);
@@ -1657,6 +1785,24 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) additive_kernel(const T* __rest
   });
 }
 
+// scale * src gathered along the lines of the LAST direction (the vol_last layout)
+template <int D, int R, typename T>
+__device__ __forceinline__ void gather_last_lines(const T* __restrict__ src, const PInfo<D>& pi, int g, T scale,
+                                                  T (&v)[R][NP]) {
+  using C = Cfg<D, T>;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int l = g + r * C::G;
+    const int i0 = l % NP, i1 = (D == 3) ? l / NP : 0;
+    const int qb = (i0 / NC) + (D == 3 ? 2 * (i1 / NC) : 0);
+    const int ob = (i0 % NC) + (D == 3 ? NC * (i1 % NC) : 0);
+    constexpr int QS = (D == 2) ? 2 : 4, SS = (D == 2) ? NC : NC * NC;
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+      v[r][j] = pi.valid ? scale * __ldg(src + (j < NC ? pi.coff[qb] : pi.coff[qb + QS]) + ob + (j % NC) * SS) : T(0);
+  }
+}
+
 // parent (coarse) cell of the colour-0 patch with lowest fine cell c0 (local):
 // along the slowest axis through the global index, so that a replicated coarse
 // level (gc.zoff = 0, full size) and a distributed one (gc.zoff = gf.zoff / 2)
@@ -1668,26 +1814,21 @@ __device__ __forceinline__ long long coarse_cell(const LevelGeom& gf, const Leve
   return D == 3 ? cell_offset_cells(gc, c0[0] >> 1, c0[1] >> 1, cs) : cell_offset_cells(gc, c0[0] >> 1, cs, 0);
 }
 
-template <typename T>
-__device__ __noinline__ void restrict_line(T* base, int stride) {
-  T v[1][NP], w[1][NC];
-  load_lines<NP, 1>(base, 0, stride, v);
-  mv<NC, NP, ProlT<T>, 1>(v, w);
-  store_lines<NC, 1>(base, 0, stride, w);
-}
-template <typename T>
-__device__ __noinline__ void prolong_line(T* base, int stride) {
-  T v[1][NC], w[1][NP];
-  load_lines<NC, 1>(base, 0, stride, v);
-  mv<NP, NC, Prol<T>, 1>(v, w);
-  store_lines<NP, 1>(base, 0, stride, w);
-}
-
-// r_c = P^T (b - hs A x) per parent cell (colour-0 patch); x == nullptr -> P^T b
+// r_c = P^T (b - hs A x) per parent cell (colour-0 patch); x == nullptr -> P^T b.
+// The residual is formed in registers on the lines of the operator's LAST pass
+// (b gathered along them, coalesced across the warp) and contracted with P^T
+// along that direction before it ever reaches shared memory; the remaining
+// directions contract the NC-wide slab (3D: y, then x), and the x-lines write
+// whole coarse-cell rows to global memory.
+#ifndef IPMG_RESTRICT_MINB
+#define IPMG_RESTRICT_MINB 0
+#endif
 template <int D, typename T>
-__global__ void __launch_bounds__(Cfg<D, T>::NT) restrict_kernel(const T* __restrict__ x, const T* __restrict__ b,
+__global__ void __launch_bounds__(Cfg<D, T>::NT, IPMG_RESTRICT_MINB) restrict_kernel(const T* __restrict__ x, const T* __restrict__ b,
                                                                  T* __restrict__ rc, LevelGeom gf, LevelGeom gc) {
   using C = Cfg<D, T>;
+  constexpr int R = C::R;
+  constexpr int LAST = D - 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* T1 = X + C::PPC * C::TSZ;
@@ -1697,104 +1838,156 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT) restrict_kernel(const T* __rest
   setup_patches<D, T>(pis, gf, 0);
   prefetch_cells<D>(b, pis, C::PPC);
   const T hs = T(gf.hs);
+  // last direction: r = b - hs (A x) on the line, then P^T along it (NC outputs)
+  auto last = [&](int p, int g, int base, int gap, int stride, const T (&yy)[R][NP]) {
+    T r[R][NP], w[R][NC];
+    gather_last_lines<D, R>(b, pis[p], g, T(1), r);
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) r[q][j] = fma_(-hs, yy[q][j], r[q][j]);
+    mv<NC, NP, ProlT<T>, R>(r, w);
+    store_lines<NC, R>(X + base, gap, stride, w);
+  };
   if (x != nullptr) {
     if (C::STAGE) stage_neighbors<D>(NB, x, pis, C::PPC);
-    T xr[C::R][NP];
+    T xr[R][NP];
     my_rows<D>(x, pis, C::PPC, T(1), xr);
     faces_prepare<D, false>(F, x, NB, pis, C::PPC);
     vol_pre<D, true>(xr, X, T1, F, pis, C::PPC);
-    vol_last<D, true>(X, T1, F, pis, C::PPC, [&](int, int, int base, int gap, int stride, const T (&yy)[C::R][NP]) {
-      store_lines<NP, C::R>(X + base, gap, stride, yy);
+    vol_last<D, true>(X, T1, F, pis, C::PPC, last);
+  } else {
+    T zero[R][NP];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) zero[q][j] = T(0);
+    for_groups<D, T>(LAST, C::PPC, [&](int p, int g, int base, int gap, int stride) { last(p, g, base, gap, stride, zero); });
+  }
+  __syncthreads();
+  if (D == 3) {   // y-lines (i0, i2 < NC): P^T along y
+    for_groups<D, T>(1, C::PPC, [&](int, int g, int base, int gap, int stride) {
+      T v[R][NP], w[R][NC];
+      load_lines<NP, R>(X + base, gap, stride, v);
+      mv<NC, NP, ProlT<T>, R>(v, w);
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if ((g + q * C::G) / NP < NC) {
+#pragma unroll
+          for (int j = 0; j < NC; ++j) X[base + q * gap + j * stride] = w[q][j];
+        }
     });
     __syncthreads();
   }
-  // residual rows r = b - hs (A x) (b rows straight from global) and P^T along x
-  // (NC outputs into the first NC entries of each row)
+  // x-lines (i1[, i2] < NC): P^T along x, one coarse-cell row straight to global
   for_groups<D, T>(0, C::PPC, [&](int p, int g, int base, int gap, int stride) {
-    T br[C::R][NP], w[C::R][NC];
-    load_rows<D, C::R>(b, pis[p], g, T(1), br);
-    if (x != nullptr) {
-      T v[C::R][NP];
-      load_lines<NP, C::R>(X + base, gap, stride, v);
-#pragma unroll
-      for (int r = 0; r < C::R; ++r)
-#pragma unroll
-        for (int j = 0; j < NP; ++j) br[r][j] = fma_(-hs, v[r][j], br[r][j]);
-    }
-    mv<NC, NP, ProlT<T>, C::R>(br, w);
-    store_lines<NC, C::R>(X + base, gap, stride, w);
-  });
-  __syncthreads();
-  // P^T along y (lines with i0 < NC), then z (lines with i0, i1 < NC)
-#pragma unroll 1
-  for (int a = 1; a < D; ++a) {
-    const int nl = (D == 2) ? NC : (a == 1 ? NC * NP : NC * NC);
-    for (int e = threadIdx.x; e < C::PPC * nl; e += blockDim.x) {
-      const int p = e / nl, li = e % nl;
-      const int l = (D == 2) ? li : (li % NC) + NP * (li / NC);
-      int base, stride;
-      if (D == 2) { base = l; stride = C::RP; }
-      else {
-        const int uu = l % NP, vv = l / NP;
-        if (a == 1) { base = uu + vv * C::PL; stride = C::RP; }
-        else        { base = uu + vv * C::RP; stride = C::PL; }
-      }
-      restrict_line<T>(X + p * C::TSZ + base, stride);
-    }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < C::PPC * C::CELL; e += blockDim.x) {
-    const int p = e / C::CELL, l = e % C::CELL;
-    if (!pis[p].valid) continue;
+    T v[R][NP], w[R][NC];
+    load_lines<NP, R>(X + base, gap, stride, v);
+    mv<NC, NP, ProlT<T>, R>(v, w);
     const PInfo<D>& pi = pis[p];
-    const long long o = coarse_cell<D>(gf, gc, pi.c0) * C::CELL + l;
-    rc[o] = X[p * C::TSZ + node_of_cell<D, T>(0, l)];
-  }
+    if (!pi.valid) return;
+    const long long cc = coarse_cell<D>(gf, gc, pi.c0) * C::CELL;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int l = g + q * C::G;
+      const int i1 = l % NP, i2 = (D == 3) ? l / NP : 0;
+      if (i1 < NC && i2 < NC) store_seg<0, T, row_vec<T>()>(rc + cc + NC * i1 + NC * NC * i2, (const T*)nullptr, T(1), &w[q][0]);
+    }
+  });
 }
 
-// x_f += P e_c per parent cell
+// x_f += P e_c per parent cell (colour-0 patch).  Expansion order (measured,
+// tools/ab_kernels.py): 2D expands the columns first, reading the coarse values
+// along y straight from global (coalesced across the warp), and adds the x
+// expansion into the fine rows with vector read-modify-writes (2D k=7 0.131 ->
+// 0.104 ms); 3D reads whole coarse-cell rows, expands x, y, and adds the z
+// expansion line-wise into the fine cells (3D k=4 0.91 -> 0.52 ms).
 template <int D, typename T>
 __global__ void __launch_bounds__(Cfg<D, T>::NT) prolong_kernel(const T* __restrict__ ec, T* __restrict__ xf,
                                                                 LevelGeom gf, LevelGeom gc) {
   using C = Cfg<D, T>;
+  constexpr int R = C::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   __shared__ PInfo<D> pis[C::PPC];
   setup_patches<D, T>(pis, gf, 0);
-  for (int e = threadIdx.x; e < C::PPC * C::CELL; e += blockDim.x) {
-    const int p = e / C::CELL, l = e % C::CELL;
-    const PInfo<D>& pi = pis[p];
-    T v = T(0);
-    if (pi.valid)
-      v = __ldg(ec + coarse_cell<D>(gf, gc, pi.c0) * C::CELL + l);
-    X[p * C::TSZ + node_of_cell<D, T>(0, l)] = v;
-  }
-  __syncthreads();
-  // expand the last direction first so that the lines of earlier directions exist
-#pragma unroll 1
-  for (int a = D - 1; a >= 1; --a) {
-    const int nl = (D == 2) ? NC : (a == 2 ? NC * NC : NC * NP);
-    for (int e = threadIdx.x; e < C::PPC * nl; e += blockDim.x) {
-      const int p = e / nl, li = e % nl;
-      const int l = (D == 2) ? li : (li % NC) + NP * (li / NC);
-      int base, stride;
-      if (D == 2) { base = l; stride = C::RP; }
-      else {
-        const int uu = l % NP, vv = l / NP;
-        if (a == 1) { base = uu + vv * C::PL; stride = C::RP; }
-        else        { base = uu + vv * C::RP; stride = C::PL; }
+  if (D == 2) {
+    // columns (i0 < NC) of the coarse cell, P along y
+    for_groups<D, T>(1, C::PPC, [&](int p, int g, int base, int gap, int stride) {
+      const PInfo<D>& pi = pis[p];
+      const long long cc = pi.valid ? coarse_cell<D>(gf, gc, pi.c0) * C::CELL : 0;
+      T v[R][NC], w[R][NP];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i0 = g + q * C::G;
+        const bool act = pi.valid && i0 < NC;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) v[q][j] = act ? __ldg(ec + cc + i0 + NC * j) : T(0);
       }
-      prolong_line<T>(X + p * C::TSZ + base, stride);
-    }
+      mv<NP, NC, Prol<T>, R>(v, w);
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (g + q * C::G < NC) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) X[base + q * gap + j * stride] = w[q][j];
+        }
+    });
     __syncthreads();
+    // x expansion, added straight into the fine rows
+    for_groups<D, T>(0, C::PPC, [&](int p, int g, int base, int gap, int stride) {
+      T v[R][NC], w[R][NP];
+      load_lines<NC, R>(X + base, gap, stride, v);
+      mv<NP, NC, Prol<T>, R>(v, w);
+      store_rows<D, 1, R>(xf, (const T*)nullptr, pis[p], g, T(1), w);
+    });
+  } else {
+    // x-lines (i1, i2 < NC): one coarse-cell row from global, P along x
+    for_groups<D, T>(0, C::PPC, [&](int p, int g, int base, int gap, int stride) {
+      const PInfo<D>& pi = pis[p];
+      const long long cc = pi.valid ? coarse_cell<D>(gf, gc, pi.c0) * C::CELL : 0;
+      T v[R][NC], w[R][NP];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int l = g + q * C::G;
+        const int i1 = l % NP, i2 = l / NP;
+        if (pi.valid && i1 < NC && i2 < NC) load_seg<T, row_vec<T>()>(ec + cc + NC * i1 + NC * NC * i2, T(1), &v[q][0]);
+        else {
+#pragma unroll
+          for (int j = 0; j < NC; ++j) v[q][j] = T(0);
+        }
+      }
+      mv<NP, NC, Prol<T>, R>(v, w);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int l = g + q * C::G;
+        if (l % NP < NC && l / NP < NC) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) X[base + q * gap + j * stride] = w[q][j];
+        }
+      }
+    });
+    __syncthreads();
+    // y-lines (i0, i2 < NC): P along y
+    for_groups<D, T>(1, C::PPC, [&](int, int g, int base, int gap, int stride) {
+      T v[R][NC], w[R][NP];
+      load_lines<NC, R>(X + base, gap, stride, v);
+      mv<NP, NC, Prol<T>, R>(v, w);
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if ((g + q * C::G) / NP < NC) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) X[base + q * gap + j * stride] = w[q][j];
+        }
+    });
+    __syncthreads();
+    // z-lines: P along z, added into the fine cells
+    for_groups<D, T>(2, C::PPC, [&](int p, int g, int base, int gap, int stride) {
+      T v[R][NC], w[R][NP];
+      load_lines<NC, R>(X + base, gap, stride, v);
+      mv<NP, NC, Prol<T>, R>(v, w);
+      store_last_lines<D, 1, R>(xf, (const T*)nullptr, pis[p], g, T(1), w);
+    });
   }
-  // x expansion, added straight into the fine rows
-  for_groups<D, T>(0, C::PPC, [&](int p, int g, int base, int gap, int stride) {
-    T v[C::R][NC], w[C::R][NP];
-    load_lines<NC, C::R>(X + base, gap, stride, v);
-    mv<NP, NC, Prol<T>, C::R>(v, w);
-    store_rows<D, 1, C::R>(xf, (const T*)nullptr, pis[p], g, T(1), w);
-  });
 }
 
 // ---------------------------------------------------------------- host side
@@ -1928,24 +2121,6 @@ cudaError_t launch_prolong(const void* ec, void* xf, const LevelGeom& gf, const 
 
 #if IPMG_DIRICHLET
 // ---------------------------------------------------------------- Dirichlet kernel (NEXT-1)
-// hinv * b gathered along the lines of the LAST direction (the vol_last layout)
-template <int D, int R, typename T>
-__device__ __forceinline__ void gather_last_lines(const T* __restrict__ src, const PInfo<D>& pi, int g, T scale,
-                                                  T (&v)[R][NP]) {
-  using C = Cfg<D, T>;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int l = g + r * C::G;
-    const int i0 = l % NP, i1 = (D == 3) ? l / NP : 0;
-    const int qb = (i0 / NC) + (D == 3 ? 2 * (i1 / NC) : 0);
-    const int ob = (i0 % NC) + (D == 3 ? NC * (i1 % NC) : 0);
-    constexpr int QS = (D == 2) ? 2 : 4, SS = (D == 2) ? NC : NC * NC;
-#pragma unroll
-    for (int j = 0; j < NP; ++j)
-      v[r][j] = pi.valid ? scale * __ldg(src + (j < NC ? pi.coff[qb] : pi.coff[qb + QS]) + ob + (j % NC) * SS) : T(0);
-  }
-}
-
 // One colour of Algorithm 1 with the Dirichlet kernel (reading
 // A20): per patch j, r = hinv b - A~ x_patch with A~ the patch operator without
 // its mesh-interior outer faces (only the patch's own cells are read -- the

@@ -10,7 +10,7 @@ pat_fn = re.compile(r"Compiling entry function '(\S+)'")
 pat_st = re.compile(r"(\d+) bytes stack frame, (\d+) bytes spill stores, (\d+) bytes spill loads")
 pat_rg = re.compile(r"Used (\d+) registers")
 only = sys.argv[1] if len(sys.argv) > 1 else ""
-for log in sorted(glob.glob(os.path.join(ROOT, "paper_2405_18982_b200", "_build", "*.log"))):
+for log in sorted(glob.glob(os.path.join(ROOT, "paper_2405_18982_b200", os.environ.get("IPMG_BUILD_DIR", "_build"), "*.log"))):
     fn = None
     st = None
     for line in open(log):
