@@ -1043,17 +1043,27 @@ __device__ __forceinline__ void trace_unit_split(T* F, const T* __restrict__ x, 
   }
 }
 
+#ifndef IPMG_TRACE_SPLIT
+#define IPMG_TRACE_SPLIT 2   // 0 never, 1 always (where the pairs fit one pass), 2 fp64 only
+#endif
+// threads the trace phase occupies when it is a single pass (0: several passes)
+template <int D, typename T>
+__host__ __device__ constexpr int trace_threads() {
+  using C = Cfg<D, T>;
+  constexpr int units = C::PPC * D * 2 * 2 * (D == 3 ? NP : 1);
+  constexpr bool split = (IPMG_TRACE_SPLIT == 1 || (IPMG_TRACE_SPLIT == 2 && sizeof(T) == 8)) && !C::STAGE &&
+                         2 * units <= C::NT;
+  return split ? 2 * units : (units <= C::NT ? units : 0);
+}
+
 template <int D, bool STAGED, bool SMOOTHER, typename T>
 __device__ __forceinline__ void face_traces(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis, int npc) {
   constexpr int NIC = (D == 3) ? NP : 1;
   constexpr int UPF = 2 * 2 * NIC;                    // units per face family: side x half x ic
   using C = Cfg<D, T>;
-#ifndef IPMG_TRACE_SPLIT
-#define IPMG_TRACE_SPLIT 2   // 0 never, 1 always (where the pairs fit one pass), 2 fp64 only
-#endif
   // measured (2D k=7): fp64 operator 0.587 -> 0.497 ms (152 -> 80 registers);
   // the fp32 smoother colour pass 0.265 -> 0.271 ms, so fp32 keeps one thread per unit
-  if ((IPMG_TRACE_SPLIT == 1 || (IPMG_TRACE_SPLIT == 2 && sizeof(T) == 8)) && !STAGED && 2 * C::PPC * D * UPF <= C::NT) {   // one pass, two threads per unit
+  if (!STAGED && trace_threads<D, T>() == 2 * C::PPC * D * UPF) {   // one pass, two threads per unit
     const int e = threadIdx.x >> 1, half = threadIdx.x & 1;
     const bool act = e < npc * D * UPF;
     const int p = act ? e / (D * UPF) : 0, r = e % (D * UPF), a = r / UPF, w = r % UPF;
@@ -1069,6 +1079,41 @@ __device__ __forceinline__ void face_traces(T* F, const T* __restrict__ x, const
     if (a == 0) trace_unit<D, 0, STAGED, SMOOTHER>(F, x, NB, pis[p], p, s, h, ic);
     else if (a == 1) trace_unit<D, 1, STAGED, SMOOTHER>(F, x, NB, pis[p], p, s, h, ic);
     else trace_unit<D, (D == 3 ? 2 : 1), STAGED, SMOOTHER>(F, x, NB, pis[p], p, s, h, ic);
+  }
+}
+
+// Face traces of all families (+ tangential transforms) and this thread's rows
+// of the first line pass (rows()).  When the trace phase is one pass that leaves
+// threads without a unit (2D fp32 k=7: 32 units for 64 threads), those threads
+// issue their row loads before the barrier, so the row latency of the idle warp
+// overlaps the trace loads instead of waiting at the barrier (IPMG_ROWS_IDLE).
+// Measured (tools/ab_kernels.py): fp32 2D k=7 operator 0.303 -> 0.267 ms, residual +
+// restriction 0.324 -> 0.291, 3D k=7 0.121 -> 0.095; the smoother loses (2D k=7 colour
+// pass 0.265 -> 0.280: 56 -> 68 registers), so it keeps the rows after the barrier.
+#ifndef IPMG_ROWS_IDLE
+#define IPMG_ROWS_IDLE 1
+#endif
+#ifndef IPMG_ROWS_IDLE_SMOOTH
+#define IPMG_ROWS_IDLE_SMOOTH 0
+#endif
+template <int D, bool SMOOTHER, typename T>
+__device__ __forceinline__ void faces_prepare(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis, int npc);
+template <int D, bool SMOOTHER, typename T>
+__device__ __forceinline__ void face_transform(T* F, const PInfo<D>* pis, int npc);
+template <int D, bool SMOOTHER, typename T, class Rows>
+__device__ __forceinline__ void faces_and_rows(T* F, const T* __restrict__ x, const T* NB, const PInfo<D>* pis,
+                                               int npc, Rows&& rows) {
+  using C = Cfg<D, T>;
+  constexpr int TT = trace_threads<D, T>();
+  if ((SMOOTHER ? IPMG_ROWS_IDLE_SMOOTH : IPMG_ROWS_IDLE) && !C::STAGE && TT > 0 && TT < C::NT) {
+    if ((int)threadIdx.x < TT) face_traces<D, false, SMOOTHER>(F, x, NB, pis, npc);
+    else rows();
+    __syncthreads();
+    face_transform<D, SMOOTHER>(F, pis, npc);
+    if ((int)threadIdx.x < TT) rows();
+  } else {
+    faces_prepare<D, SMOOTHER>(F, x, NB, pis, npc);
+    rows();
   }
 }
 
@@ -1628,9 +1673,10 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_VMULT) vmult_ke
 #ifdef IPMG_ROWS_EARLY
   my_rows<D>(x, pis, C::PPC, T(1), xr);        // in flight while the traces load
 #endif
-  faces_prepare<D, false>(F, x, NB, pis, C::PPC);
 #ifndef IPMG_ROWS_EARLY
-  my_rows<D>(x, pis, C::PPC, T(1), xr);
+  faces_and_rows<D, false>(F, x, NB, pis, C::PPC, [&] { my_rows<D>(x, pis, C::PPC, T(1), xr); });
+#else
+  faces_prepare<D, false>(F, x, NB, pis, C::PPC);
 #endif
   vol_pre<D, true>(xr, X, T1, F, pis, C::PPC);
   const T hs = T(g.hs);
@@ -1752,9 +1798,13 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, Cfg<D, T>::MINB_SMOOTH)
     store_rows<D, 0, C::R>(x_out, (const T*)nullptr, pis[p], gg, T(1), w);
   };
   if (x_in != nullptr) {
+#if IPMG_TMA_B || defined(IPMG_ROWS_EARLY)
     faces_prepare<D, true>(F, x_in, NB, pis, C::PPC);
 #ifndef IPMG_ROWS_EARLY   // measured: loading the rows after the traces keeps registers low
     IPMG_MY_B_ROWS();
+#endif
+#else
+    faces_and_rows<D, true>(F, x_in, NB, pis, C::PPC, [&] { IPMG_MY_B_ROWS(); });
 #endif
     fd_pre<D, true>(br, X, F, pis, C::PPC);
     fd_post<D, true>(X, F, pis, C::PPC, out);
@@ -1852,8 +1902,7 @@ __global__ void __launch_bounds__(Cfg<D, T>::NT, IPMG_RESTRICT_MINB) restrict_ke
   if (x != nullptr) {
     if (C::STAGE) stage_neighbors<D>(NB, x, pis, C::PPC);
     T xr[R][NP];
-    my_rows<D>(x, pis, C::PPC, T(1), xr);
-    faces_prepare<D, false>(F, x, NB, pis, C::PPC);
+    faces_and_rows<D, false>(F, x, NB, pis, C::PPC, [&] { my_rows<D>(x, pis, C::PPC, T(1), xr); });
     vol_pre<D, true>(xr, X, T1, F, pis, C::PPC);
     vol_last<D, true>(X, T1, F, pis, C::PPC, last);
   } else {
