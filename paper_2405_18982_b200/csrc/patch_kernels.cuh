@@ -120,8 +120,12 @@ struct Cfg {
   // R = 1); 4 warps for k <= 2,
   // whose tiny patches otherwise leave a CTA with too little work (C3 sweep: 3D
   // k=2 smoother step 10.4 -> 12.7 GDoF/s)
+#ifndef IPMG_GT64
+#define IPMG_GT64 IPMG_GROUPS_TARGET
+#endif
   static constexpr int GT = NC <= 3 ? 4 * IPMG_GROUPS_TARGET
-                                    : ((sizeof(T) == 4 && R == 1) ? 2 * IPMG_GROUPS_TARGET : IPMG_GROUPS_TARGET);
+                                    : ((sizeof(T) == 4 && R == 1) ? 2 * IPMG_GROUPS_TARGET
+                                                                  : (sizeof(T) == 8 ? IPMG_GT64 : IPMG_GROUPS_TARGET));
   static constexpr int PPC = (GT / G) > 1 ? (GT / G) : 1;   // patches per CTA
   static constexpr int GROUPS = PPC * G;
   static constexpr int NT = (((GROUPS + 31) / 32) * 32) > 256 ? 256 : ((GROUPS + 31) / 32) * 32;
