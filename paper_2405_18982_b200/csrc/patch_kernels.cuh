@@ -425,7 +425,15 @@ __device__ __forceinline__ void mv_acc(const T (&in)[R][NIN], T (&out)[R][NOUT],
 // pairs (i, i+1) from a column pair of the matrix (one 64-bit uniform-register
 // constant) times a broadcast input: half the FMA instructions of the scalar
 // form -- the smoother is issue-bound, so this is the main fp32 lever.
+#ifndef IPMG_FFMA2_BUILTIN
+#define IPMG_FFMA2_BUILTIN 1
+#endif
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+#if IPMG_FFMA2_BUILTIN
+  // the sm_100 builtin: the compiler sees the operation, so broadcast inputs
+  // become the .F32 operand form instead of MOV/LOP3 register-pair packing
+  return __ffma2_rn(a, b, c);
+#endif
   unsigned long long ra, rb, rc, rd;
   ra = (unsigned long long)__float_as_uint(a.x) | ((unsigned long long)__float_as_uint(a.y) << 32);
   rb = (unsigned long long)__float_as_uint(b.x) | ((unsigned long long)__float_as_uint(b.y) << 32);
