@@ -233,8 +233,13 @@ __device__ __forceinline__ T fma_(T a, T b, T c) { return fma(a, b, c); }
 
 // interior patches (variant 0, the overwhelming majority) take the path with
 // compile-time constant operands; boundary patches the register-indexed one
+#ifdef IPMG_TIMING_FAST_ONLY   // timing experiment only: wrong on boundary patches
+#define IPMG_VAR_SPLIT(var, FAST, SLOW) \
+  { (void)(var); FAST; }
+#else
 #define IPMG_VAR_SPLIT(var, FAST, SLOW) \
   if ((var) == 0) { FAST; } else { const int v_ = (var); SLOW; }
+#endif
 // reciprocal of a positive eigenvalue sum: MUFU approximation (fp32: 1 ulp);
 // fp64: approximation refined by two Newton steps (full precision)
 __device__ __forceinline__ float rcp_(float x) {
