@@ -69,6 +69,9 @@ struct TabData {
   alignas(16) T LP[4][NP][RP];      // 2-cell patch stiffness + face terms, variant v
   alignas(16) T S[4][NP][RP];       // eigenvectors, S[v][node][mode]
   alignas(16) T ST[4][NP][RP];      // transposed eigenvectors, ST[v][mode][node]
+  alignas(16) T SO[NP][RC];         // odd-mode columns of S[0]: SO[node][m] = S[0][node][NP/2 + m], rows
+                                    // 16-byte aligned so that output pairs (2q, 2q+1) are aligned 8-byte
+                                    // constants also when NP/2 is odd (even k)
   alignas(16) T MS[4][NP][RP];      // M^P S = (S^T M^P)^T: face arrays of directions already in eigen-space
   alignas(16) T CF[4][RP];          // face coupling coefficients along the normal (C x_ext):
                                     // 0 low/u, 1 low/u', 2 high/u, 3 high/u'  (see face_* kernels)

@@ -296,7 +296,16 @@ struct EvenT {   // (S_e^T)[m][i] = S[0][i][m],      m, i < np/2
 };
 template <typename T>
 struct OddT {    // (S_o^T)[m][i] = S[0][i][np/2+m]
+#ifndef IPMG_ODD_ALIGNED
+#define IPMG_ODD_ALIGNED 1
+#endif
+#if IPMG_ODD_ALIGNED
+  // aligned copy: with S[0][i][NP/2 + m] the pairs straddle 8-byte boundaries for odd
+  // NP/2 and cost one UMOV per constant (3D k=4: ~20 per line pass)
+  static __device__ __forceinline__ T get(int m, int i) { return tab<T>().SO[i][m]; }
+#else
   static __device__ __forceinline__ T get(int m, int i) { return tab<T>().S[0][i][NP / 2 + m]; }
+#endif
   static __device__ __forceinline__ constexpr bool nz(int, int) { return true; }
 };
 template <typename T>
@@ -2281,6 +2290,7 @@ void fill_tab(TabData<K, T>& t, const FE1D& fe) {
         t.LP[v][i][j] = (T)LPv[i * NP + j];
         t.S[v][i][j] = (T)Sv[i * NP + j];
         t.ST[v][j][i] = (T)Sv[i * NP + j];
+        if (v == 0 && j >= NP / 2) t.SO[i][j - NP / 2] = (T)Sv[i * NP + j];
       }
     for (int i = 0; i < NP; ++i) {
       t.lam[v][i] = (T)(kDir ? fe.lamD[v][i] : fe.lam[v][i]);
