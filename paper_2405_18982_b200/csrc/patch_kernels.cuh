@@ -1183,7 +1183,26 @@ __device__ __forceinline__ void face_transform(T* F, const PInfo<D>* pis, int np
     }
     __syncthreads();
   }
-  if (D == 3) {                                   // second tangential direction
+#ifndef IPMG_FACE_LINE_INLINE
+#define IPMG_FACE_LINE_INLINE 1
+#endif
+  if (D == 3 && IPMG_FACE_LINE_INLINE && !any1 && C::PPC * D * 4 * NP <= C::NT) {
+    // one pass (a line per thread): the tangential mass inline, no call; modes are
+    // 0 (skip) or 1 (block-diagonal mass, compile-time constants) here
+    const int e = threadIdx.x;
+    if (e < npc * D * 4 * NP) {
+      const int o = e % NP, arr = e / NP;
+      const int a = (arr / 4) % D, p = arr / (4 * D);
+      if (face_mode<SMOOTHER>(a, second_tan(a)) == 1) {
+        T* base = F + p * C::FSZ + (arr % (4 * D)) * C::FARR + o;
+        T v[1][NP], w[1][NP];
+        load_lines<NP, 1>(base, 0, C::FROW, v);
+        mv<NP, NP, MassP<T>, 1>(v, w);
+        store_lines<NP, 1>(base, 0, C::FROW, w);
+      }
+    }
+    __syncthreads();
+  } else if (D == 3) {                            // second tangential direction
 #pragma unroll 1
     for (int e = threadIdx.x; e < npc * D * 4 * NP; e += blockDim.x) {
       const int o = e % NP, arr = e / NP;
