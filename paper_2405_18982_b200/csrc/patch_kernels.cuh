@@ -126,9 +126,17 @@ struct Cfg {
   static constexpr int GT = NC <= 3 ? 4 * IPMG_GROUPS_TARGET
                                     : ((sizeof(T) == 4 && R == 1) ? 2 * IPMG_GROUPS_TARGET
                                                                   : (sizeof(T) == 8 ? IPMG_GT64 : IPMG_GROUPS_TARGET));
-  static constexpr int PPC = (GT / G) > 1 ? (GT / G) : 1;   // patches per CTA
+#ifndef IPMG_PPC3
+#define IPMG_PPC3 0   // > 0: patches per CTA in 3D (experiments)
+#endif
+#ifndef IPMG_PPC3_NC
+#define IPMG_PPC3_NC 0   // restrict IPMG_PPC3 to this NC (0: all)
+#endif
+  static constexpr int PPC = (D == 3 && IPMG_PPC3 > 0 && (IPMG_PPC3_NC == 0 || IPMG_PPC3_NC == NC))
+                                 ? IPMG_PPC3
+                                 : ((GT / G) > 1 ? (GT / G) : 1);   // patches per CTA
   static constexpr int GROUPS = PPC * G;
-  static constexpr int NT = (((GROUPS + 31) / 32) * 32) > 256 ? 256 : ((GROUPS + 31) / 32) * 32;
+  static constexpr int NT = (((GROUPS + 31) / 32) * 32) > 1024 ? 1024 : ((GROUPS + 31) / 32) * 32;
 
   // line base offset of group g (first line) of patch p for direction a
   static constexpr int line_base(int a, int p, int g, int pl, int tsz) {
