@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double* __r
 // r32 != nullptr: also r32 = (float) r (the fp32 V-cycle input).
 // VEC: 16-byte (double2) accesses, two pairs per thread and iteration in flight
 // (the scalar grid-stride loop kept ~30 KB per SM in flight: 5.2 TB/s under ncu)
-template <bool VEC>
+template <bool VEC, bool DOX>
 __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                                              const double* __restrict__ p, const double* __restrict__ q,
                                                              long long n, const double* __restrict__ sc, int i_rz,
@@ -71,13 +71,19 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
     for (long long i = t0; i < n2; i += 2 * nt) {
       const long long j = i + nt;
       const bool two = j < n2;
-      const double2 xa = x2[i], pa = __ldg(p2 + i), qa = __ldg(q2 + i), ra = r2[i];
-      double2 xb, pb, qb, rb;
-      if (two) { xb = x2[j]; pb = __ldg(p2 + j); qb = __ldg(q2 + j); rb = r2[j]; }
+      double2 xa{}, pa{}, xb{}, pb{};
+      if (DOX) { xa = x2[i]; pa = __ldg(p2 + i); }
+      const double2 qa = __ldg(q2 + i), ra = r2[i];
+      double2 qb, rb;
+      if (two) {
+        if (DOX) { xb = x2[j]; pb = __ldg(p2 + j); }
+        qb = __ldg(q2 + j);
+        rb = r2[j];
+      }
       double2 ro;
       ro.x = fma(-alpha, qa.x, ra.x);
       ro.y = fma(-alpha, qa.y, ra.y);
-      x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+      if (DOX) x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
       r2[i] = ro;
       if (r32) f2[i] = make_float2((float)ro.x, (float)ro.y);
       s = fma(ro.x, ro.x, s);
@@ -85,7 +91,7 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
       if (two) {
         ro.x = fma(-alpha, qb.x, rb.x);
         ro.y = fma(-alpha, qb.y, rb.y);
-        x2[j] = make_double2(fma(alpha, pb.x, xb.x), fma(alpha, pb.y, xb.y));
+        if (DOX) x2[j] = make_double2(fma(alpha, pb.x, xb.x), fma(alpha, pb.y, xb.y));
         r2[j] = ro;
         if (r32) f2[j] = make_float2((float)ro.x, (float)ro.y);
         s = fma(ro.x, ro.x, s);
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
     done = n2 << 1;
   }
   for (long long i = done + t0; i < n; i += nt) {
-    x[i] = fma(alpha, p[i], x[i]);
+    if (DOX) x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     if (r32) r32[i] = (float)ri;
@@ -111,6 +117,41 @@ __global__ void cg_p32_kernel(double* __restrict__ p, const float* __restrict__ 
   const double beta = i_old < 0 ? 0.0 : sc[i_new] / sc[i_old];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = i_old < 0 ? (double)z[i] : fma(beta, p[i], (double)z[i]);
+}
+
+// deferred CG solution update fused with the direction update (mixed precision):
+// x += alpha p_old (alpha = s[i_rz] / s[i_pq], the step cg_xr_kernel took with
+// DOX = false), then p = (double) z32 + beta p_old (beta = s[i_new] / s[i_rz]).
+// The same fma on the same p_old as in cg_xr_kernel: x is bit-identical, and the
+// x/p streams are read once instead of twice per iteration.
+template <bool VEC>
+__global__ void cg_xp32_kernel(double* __restrict__ x, double* __restrict__ p, const float* __restrict__ z,
+                               long long n, const double* __restrict__ sc, int i_new, int i_rz, int i_pq) {
+  const double alpha = sc[i_rz] / sc[i_pq], beta = sc[i_new] / sc[i_rz];
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+  const long long n2 = VEC ? n >> 1 : 0;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  const float2* z2 = reinterpret_cast<const float2*>(z);
+  for (long long i = t0; i < n2; i += nt) {
+    const double2 xo = x2[i], po = p2[i];
+    const float2 zz = __ldg(z2 + i);
+    x2[i] = make_double2(fma(alpha, po.x, xo.x), fma(alpha, po.y, xo.y));
+    p2[i] = make_double2(fma(beta, po.x, (double)zz.x), fma(beta, po.y, (double)zz.y));
+  }
+  for (long long i = (n2 << 1) + t0; i < n; i += nt) {
+    const double po = p[i];
+    x[i] = fma(alpha, po, x[i]);
+    p[i] = fma(beta, po, (double)z[i]);
+  }
+}
+
+// x += alpha p (alpha = s[i_rz] / s[i_pq]): the deferred update of the last step
+__global__ void cg_x_kernel(double* __restrict__ x, const double* __restrict__ p, long long n,
+                            const double* __restrict__ sc, int i_rz, int i_pq) {
+  const double alpha = sc[i_rz] / sc[i_pq];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = fma(alpha, p[i], x[i]);
 }
 
 // p = z + beta p, beta = s[i_new] / s[i_old]
@@ -333,8 +374,28 @@ cudaError_t cg_update_xr(double* x, double* r, const double* p, const double* q,
   const bool vec = ((reinterpret_cast<unsigned long long>(x) | reinterpret_cast<unsigned long long>(r) |
                      reinterpret_cast<unsigned long long>(p) | reinterpret_cast<unsigned long long>(q)) & 15) == 0 &&
                    (reinterpret_cast<unsigned long long>(r32) & 7) == 0;
-  if (vec) cg_xr_kernel<true><<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
-  else cg_xr_kernel<false><<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
+  if (x == nullptr) {   // solution update deferred (cg_update_xp32 / cg_update_x)
+    if (vec) cg_xr_kernel<true, false><<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
+    else cg_xr_kernel<false, false><<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
+  } else {
+    if (vec) cg_xr_kernel<true, true><<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
+    else cg_xr_kernel<false, true><<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, sc, i_rz, i_pq, partial, r32);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t cg_update_xp32(double* x, double* p, const float* z, long long n, const double* sc, int i_new, int i_rz,
+                           int i_pq, cudaStream_t s) {
+  const bool vec = ((reinterpret_cast<unsigned long long>(x) | reinterpret_cast<unsigned long long>(p)) & 15) == 0 &&
+                   (reinterpret_cast<unsigned long long>(z) & 7) == 0;
+  if (vec) cg_xp32_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(x, p, z, n, sc, i_new, i_rz, i_pq);
+  else cg_xp32_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(x, p, z, n, sc, i_new, i_rz, i_pq);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_update_x(double* x, const double* p, long long n, const double* sc, int i_rz, int i_pq,
+                        cudaStream_t s) {
+  cg_x_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, p, n, sc, i_rz, i_pq);
   return cudaGetLastError();
 }
 

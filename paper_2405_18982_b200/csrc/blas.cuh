@@ -22,6 +22,12 @@ cudaError_t cg_update_xr(double* x, double* r, const double* p, const double* q,
                          int i_rz, int i_pq, double* partial, cudaStream_t s, float* r32 = nullptr);
 cudaError_t cg_update_p32(double* p, const float* z, long long n, const double* sc, int i_new, int i_old,
                           cudaStream_t s);
+// x += alpha p_old ; p = z32 + beta p_old  (alpha = sc[i_rz]/sc[i_pq], beta = sc[i_new]/sc[i_rz])
+cudaError_t cg_update_xp32(double* x, double* p, const float* z, long long n, const double* sc, int i_new, int i_rz,
+                           int i_pq, cudaStream_t s);
+// x += alpha p  (alpha = sc[i_rz]/sc[i_pq])
+cudaError_t cg_update_x(double* x, const double* p, long long n, const double* sc, int i_rz, int i_pq,
+                        cudaStream_t s);
 cudaError_t cg_update_p(double* p, const double* z, long long n, const double* sc, int i_new, int i_old,
                         cudaStream_t s);
 cudaError_t cast_f2d_dot(const float* zf, double* zd, const double* r, long long n, double* partial, cudaStream_t s);

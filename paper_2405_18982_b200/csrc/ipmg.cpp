@@ -976,8 +976,11 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       h->n_launches += 3;
       CK(ipmg::finalize(h->partial, h->scal + 2, s, nparts), "finalize");
       if ((st = h->allsum(h->scal + 2)) != IPMG_OK) return st;
-      TK(ipmg::cg_update_xr(x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s, r32),
-         (48.0 + (r32 ? 4.0 : 0.0)) * n, "update");
+      // mixed: the solution update x += alpha p is deferred into the next direction
+      // update (cg_update_xp32), or the final cg_update_x on convergence -- the same
+      // fma on the same p, one pass over x and p fewer per iteration
+      TK(ipmg::cg_update_xr(mixed ? nullptr : x, h->r, h->p, h->q, n, h->scal, cur, 2, h->partial, s, r32),
+         (mixed ? 28.0 : 48.0) * n, "update");
       CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
       if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
       CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
@@ -986,7 +989,11 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       ++it;
       const double rn = std::sqrt(h->hpin[0]);
       hist.push_back(rn);
-      if (rn <= rtol * r0) { conv = true; break; }
+      if (rn <= rtol * r0) {
+        conv = true;
+        if (mixed) TK(ipmg::cg_update_x(x, h->p, n, h->scal, cur, 2, s), 24.0 * n, "update x");
+        break;
+      }
       if (mixed) {
         st = h->vcycle_level(L, IPMG_FP32);
         if (st != IPMG_OK) return st;
@@ -994,7 +1001,7 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
         TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
         CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
         if ((st = h->allsum(h->scal + (1 - cur))) != IPMG_OK) return st;
-        TK(ipmg::cg_update_p32(h->p, z32, n, h->scal, 1 - cur, cur, s), 20.0 * n, "update p");
+        TK(ipmg::cg_update_xp32(x, h->p, z32, n, h->scal, 1 - cur, cur, 2, s), 36.0 * n, "update x, p");
       } else {
         st = h->vcycle(h->r, h->z, h->partial);
         if (st != IPMG_OK) return st;
