@@ -31,7 +31,22 @@ __global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const TA* __re
                                                                    long long n, double* __restrict__ partial) {
   __shared__ double sh[32];
   double s = 0.0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+  long long start = 0;
+  if (sizeof(TA) == 8 && sizeof(TB) == 4 &&
+      ((reinterpret_cast<unsigned long long>(a) & 15) | (reinterpret_cast<unsigned long long>(b) & 7)) == 0) {
+    // r . z32 of the mixed PCG: double2 / float2 accesses
+    const long long n2 = n >> 1;
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const float2* b2 = reinterpret_cast<const float2*>(b);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+      const double2 u = __ldg(a2 + i);
+      const float2 v = __ldg(b2 + i);
+      s = fma(u.x, (double)v.x, s);
+      s = fma(u.y, (double)v.y, s);
+    }
+    start = n2 << 1;
+  }
+  for (long long i = start + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     s = fma((double)a[i], (double)b[i], s);
   s = block_sum<double>(s, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
@@ -133,11 +148,20 @@ __global__ void cg_xp32_kernel(double* __restrict__ x, double* __restrict__ p, c
   double2* x2 = reinterpret_cast<double2*>(x);
   double2* p2 = reinterpret_cast<double2*>(p);
   const float2* z2 = reinterpret_cast<const float2*>(z);
-  for (long long i = t0; i < n2; i += nt) {
+  for (long long i = t0; i < n2; i += 2 * nt) {   // two pairs in flight per thread
+    const long long j = i + nt;
+    const bool two = j < n2;
     const double2 xo = x2[i], po = p2[i];
     const float2 zz = __ldg(z2 + i);
+    double2 xo2{}, po2{};
+    float2 zz2{};
+    if (two) { xo2 = x2[j]; po2 = p2[j]; zz2 = __ldg(z2 + j); }
     x2[i] = make_double2(fma(alpha, po.x, xo.x), fma(alpha, po.y, xo.y));
     p2[i] = make_double2(fma(beta, po.x, (double)zz.x), fma(beta, po.y, (double)zz.y));
+    if (two) {
+      x2[j] = make_double2(fma(alpha, po2.x, xo2.x), fma(alpha, po2.y, xo2.y));
+      p2[j] = make_double2(fma(beta, po2.x, (double)zz2.x), fma(beta, po2.y, (double)zz2.y));
+    }
   }
   for (long long i = (n2 << 1) + t0; i < n; i += nt) {
     const double po = p[i];
