@@ -27,7 +27,11 @@
  *    ipmg_from_cellwise convert to/from plain cell-wise lexicographic order.
  *  - Work is enqueued on cfg.cuda_stream (NULL = legacy default stream) and
  *    calls return without synchronising, except ipmg_cg_solve (it reads the
- *    residual norm every iteration) and the host-only utilities.
+ *    residual norm every iteration) and the host-only utilities.  Results of
+ *    every call, the solvers' x included, are complete in stream order on
+ *    cfg.cuda_stream: the mixed-precision CG applies its last solution update
+ *    after the final residual check, so read x on that stream (or after
+ *    ipmg_synchronize), as for every other output.
  *  - A handle must not be used by two host threads at once.
  */
 #ifndef IPMG_H
