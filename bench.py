@@ -1,24 +1,32 @@
 #!/usr/bin/env python
-"""Benchmark of the GMG-preconditioned CG hot path (BASELINE.json metric
-"GDoF/s of operator vmult and smoother step; GMG-CG time-to-solution +
-iterations") on BASELINE.json configs[1]: 2D Poisson SIPG, k = 7, 1024^2
-cells (67,108,864 dofs), 10 levels, multiplicative vertex-patch smoother with
-the full kernel, fp32 V-cycle inside fp64 CG (mixed).
+"""Benchmark of the GMG-preconditioned CG hot path (BASELINE.json metric "GDoF/s of
+operator vmult and smoother step; GMG-CG time-to-solution + iterations").
 
-One "step" = one complete GMG-CG solve A x = b to ||r|| <= 1e-8 ||b|| with
-f == 1 -- every row of SURVEY.md 8(a): operator apply, smoother
-colour passes, residual+restriction, prolongation, coarse solve, V-cycle, PCG.
-value = dofs solved per second over the timed steps (GDoF/s).
+Headline workload = BASELINE.json configs[3] (C4), the north star's target solve, at N GPUs:
+3D Poisson SIPG, k = 4, the box (0,1)^2 x (0,1/2) with T_0 = 2x2x1 cubic cells, 8 levels,
+finest mesh 256x256x128 cells = 1,048,576,000 dofs (Fig. 11-13 Q4 3D;
+SURVEY.md 8(d) C4), multiplicative full-kernel vertex-patch smoother, fp32 V-cycle inside
+fp64 CG, f == 1, x0 = 0, ||r|| <= 1e-8 ||b||.  C4 is the largest
+single-GPU configuration of BASELINE.json; N > 1 runs it slab-decomposed (strong scaling).
+C2 (2D k=7, 67M dofs, configs[1]) is reported as a secondary line item.
+
+One "step" = one complete GMG-CG solve -- every row of SURVEY.md 8(a): operator apply,
+smoother colour passes, residual+restriction, prolongation, coarse solve, V-cycle, PCG.
+value = dofs solved per second over the K timed steps (GDoF/s), inputs resident in HBM
+(8.4 GB fp64 vectors >> 126 MB L2, no flush needed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Rank 0 prints one JSON line.  --impl reference times the CPU oracle
-(oracle/, numpy/scipy, 1 BLAS thread) on a bounded sample of the same workload
-(the paper has no runnable reference implementation).
+--gpus N > 1 without torchrun re-executes itself under torch.distributed.run (one rank per
+GPU, 127.0.0.1).  Rank 0 prints one JSON line.  --impl reference times the CPU oracle
+(oracle/, numpy/scipy) on a bounded sample of the same workload on all host cores (the paper
+has no runnable reference implementation).
 """
 import argparse
 import json
+import multiprocessing as mp
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -28,33 +36,35 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(name="C2", dim=2, degree=7, n_levels=10, coarse=(2, 2),
-                desc="2D Poisson SIPG k=7, 1024x1024 cells, 67,108,864 dofs, 10 levels, f=1, "
-                     "multiplicative full-kernel vertex-patch smoother, fp32 V-cycle / fp64 CG (BASELINE.json configs[1])")
-# bounded oracle sample: same method and degree on a smaller mesh (64x64 cells)
-CPU_SAMPLE = dict(dim=2, degree=7, n_levels=6)
 METRIC = "GDoF/s of operator vmult and smoother step; GMG-CG time-to-solution + iterations"
 UNIT = "GDoF/s (GMG-CG solve: dofs / time-to-solution)"
+C4 = dict(name="C4", dim=3, degree=4, n_levels=8, coarse=(2, 2, 1),
+          desc="3D Poisson SIPG k=4, (0,1)^2x(0,1/2), T_0 = 2x2x1 cells, 8 levels, finest 256x256x128 cells, "
+               "1,048,576,000 dofs, f=1, multiplicative full-kernel vertex-patch smoother, fp32 V-cycle / fp64 CG, "
+               "rtol 1e-8 (BASELINE.json configs[3])")
+C2 = dict(name="C2", dim=2, degree=7, n_levels=10, coarse=(2, 2),
+          desc="2D Poisson SIPG k=7, 1024x1024 cells, 67,108,864 dofs, 10 levels (BASELINE.json configs[1])")
+WORKLOAD = C4
+# bounded oracle sample: the same method, degree, box and solver on the 3-level mesh of the
+# C4 hierarchy (8x8x4 cells, 32,000 dofs); one solve ~1 s of one core
+CPU_SAMPLE = dict(dim=3, degree=4, n_levels=3, coarse=(2, 2, 1))
 
 
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------- roofline model
 def smoother_flops_per_dof(dim, k):
-    """Algorithmic flops of one full-kernel colour pass per dof (DESIGN.md
-    "Roofline"), for the algorithm the kernel runs: fast diagonalisation with
-    the even/odd factorised interior eigenbasis -- 2d line transforms of
-    np^(d-1) lines each costing np^2/2 FMAs (two (np/2)^2 halves) + np adds,
-    and one eigenvalue scaling per patch dof -- plus the face coupling (trace
-    value/derivative, tangential mass, S^T M transforms, injection), counted per
-    patch and divided by the patch dofs.  (The dense-eigenbasis model of
-    SURVEY.md 8(d), 2d np^2 FMAs per line, is twice the FD term.)"""
+    """Algorithmic flops of one full-kernel colour pass per covered dof for the algorithm
+    the kernel runs (model "even/odd"): fast diagonalisation with the
+    even/odd factorised interior eigenbasis -- 2d line transforms of np^(d-1) lines, each
+    np^2/2 FMAs (two (np/2)^2 halves) + np adds, one eigenvalue scaling per patch dof -- plus
+    the face coupling (trace value/derivative, tangential masses, injection) per patch."""
     nc, np_ = k + 1, 2 * (k + 1)
     patch = np_ ** dim
     nfp = np_ ** (dim - 1)
@@ -63,12 +73,15 @@ def smoother_flops_per_dof(dim, k):
     return (fd + dim * per_dir) / patch
 
 
-def alu_peak_tflops(prec, peaks):
-    """CUDA-core peak from the unit counts and the max SM clock
-    (B200: 148 SMs x 128 FP32 lanes, FP64 at half rate; 2 flops per FMA)."""
-    mhz = peaks.get("sm_max_mhz", 1965.0)
-    lanes = 128 if prec == "fp32" else 64
-    return 148 * lanes * 2 * mhz * 1e6 / 1e12
+def smoother_flops_per_dof_dense(dim, k):
+    """SURVEY.md 8(d) dense-eigenbasis model of the replacement form, per covered dof and
+    colour pass: 8d(k+1) + 30 (3D); 2D: 8d(k+1) + 20."""
+    return 8 * dim * (k + 1) + (30 if dim == 3 else 20)
+
+
+def vmult_flops_per_dof(dim, k):
+    """3D 14(k+1) + 48, 2D 8(k+1) + 24 (dense 1D contractions)."""
+    return 14 * (k + 1) + 48 if dim == 3 else 8 * (k + 1) + 24
 
 
 # ---------------------------------------------------------------- clocks
@@ -117,97 +130,151 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- distributed
-def dist_init(backend):
+def maybe_respawn(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (one rank per GPU)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        sys.exit("bench.py: --gpus %d but only %d CUDA devices visible" % (args.gpus, torch.cuda.device_count()))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws <= 1:
         return 0, 1, 0
+    import torch
     import torch.distributed as dist
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    if backend == "nccl":
-        import torch
-        torch.cuda.set_device(local)
-    dist.init_process_group(backend)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
     return rank, ws, local
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def oracle_sample_solve():
-    """Set up the oracle on the bounded sample; returns (solve_fn, ndofs).
-    Setup (assembly, patch LU factorisations) is excluded from timing, as on
-    the GPU."""
-    from oracle import assemble, krylov, multigrid
-    V = multigrid.VCycle(CPU_SAMPLE["dim"], CPU_SAMPLE["degree"], CPU_SAMPLE["n_levels"], dtype=np.float32)
-    L = CPU_SAMPLE["n_levels"] - 1
-    A = V.A64[L]
-    b = assemble.rhs(V.levels[L], CPU_SAMPLE["degree"])
-
-    def solve():
-        x, hist, conv = krylov.pcg(A, b, V, rtol=1e-8)
-        return len(hist) - 1
-    return solve, A.shape[0]
+_SAMPLE = {}
 
 
-def cpu_threads_limit():
-    """Pin every BLAS/OpenMP pool to 1 thread.  The libraries must be loaded
-    first: threadpoolctl only limits pools that exist when it is called."""
+def _sample_setup():
+    """Oracle set-up on the bounded sample (excluded from timing, as on the GPU)."""
+    from oracle import assemble, multigrid
+    s = CPU_SAMPLE
+    V = multigrid.VCycle(s["dim"], s["degree"], s["n_levels"], n0=s["coarse"], dtype=np.float32)
+    L = s["n_levels"] - 1
+    _SAMPLE.update(V=V, A=V.A64[L], b=assemble.rhs(V.levels[L], s["degree"]))
+    return V.A64[L].shape[0]
+
+
+def _sample_solve():
+    from oracle import krylov
+    x, hist, conv = krylov.pcg(_SAMPLE["A"], _SAMPLE["b"], _SAMPLE["V"], rtol=1e-8)
+    assert conv
+    return len(hist) - 1
+
+
+def _worker(barrier, n_warm, n_solves, q):
+    for _ in range(n_warm):
+        _sample_solve()
+    barrier.wait()
+    its = 0
+    for _ in range(n_solves):
+        its = _sample_solve()
+    q.put(its)
+
+
+def host_cores():
     try:
-        import scipy.linalg  # noqa: F401
-        import scipy.sparse.linalg  # noqa: F401
-        from oracle import multigrid  # noqa: F401
-        from threadpoolctl import threadpool_limits
-        return threadpool_limits(limits=1)
+        return len(os.sched_getaffinity(0))
     except Exception:
-        return None
+        return os.cpu_count() or 1
 
 
-def sample_desc():
-    n = 2 ** (CPU_SAMPLE["n_levels"])
-    return ("oracle GMG-CG solve (numpy/scipy, fp32 V-cycle, 1 BLAS thread) on 2D k=%d, %dx%d cells, "
-            "%d levels, %d dofs; setup excluded" % (CPU_SAMPLE["degree"], n, n, CPU_SAMPLE["n_levels"],
-                                                    n * n * (CPU_SAMPLE["degree"] + 1) ** 2))
+def sample_desc(workers):
+    s = CPU_SAMPLE
+    cells = [c * 2 ** (s["n_levels"] - 1) for c in s["coarse"]]
+    n = int(np.prod(cells)) * (s["degree"] + 1) ** s["dim"]
+    return ("oracle GMG-CG solve (numpy/scipy CSR SpMV + dense patch LU, fp32 V-cycle, fp64 CG) on 3D k=%d, "
+            "%s cells (levels 0..%d of the C4 hierarchy), %d dofs; %d independent solves in parallel, one per "
+            "host core (forked processes, 1 BLAS thread each); setup excluded"
+            % (s["degree"], "x".join(map(str, cells)), s["n_levels"] - 1, n, workers))
 
 
-def run_cpu_baseline(reps=1):
-    lim = cpu_threads_limit()
-    solve, n = oracle_sample_solve()
-    t = []
-    its = 0
-    for _ in range(reps):
+def run_oracle_parallel(n_solves, n_warm=0, workers=None):
+    """Oracle throughput on all host cores: `workers` forked processes (copy-on-write
+    oracle set-up) each run n_warm untimed and then n_solves timed sample solves;
+    value = total dofs of the timed solves / wall time from the common start barrier to
+    the last worker's end."""
+    from threadpoolctl import threadpool_limits
+    workers = workers or host_cores()
+    with threadpool_limits(limits=1):
+        n = _sample_setup()
+        ctx = mp.get_context("fork")
+        barrier = ctx.Barrier(workers + 1)
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_worker, args=(barrier, n_warm, n_solves, q)) for _ in range(workers)]
+        for p in procs:
+            p.start()
+        barrier.wait()
         t0 = time.perf_counter()
-        its = solve()
-        t.append(time.perf_counter() - t0)
-    del lim
-    sec = float(np.median(t))
-    return {"value": n / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample_desc(),
-            "seconds_per_solve": sec, "iterations": its}
+        its = [q.get() for _ in procs]
+        sec = time.perf_counter() - t0
+        for p in procs:
+            p.join()
+    return {"value": workers * n_solves * n / sec / 1e9, "unit": UNIT, "cores": workers, "kind": "oracle",
+            "sample": sample_desc(workers), "seconds": sec, "solves": workers * n_solves,
+            "seconds_per_round": sec / n_solves, "iterations": its[0]}
 
 
-def run_reference(args, rank, ws):
-    if rank != 0:
+def run_reference(args):
+    """The reference arm: the oracle as it stands, W warm-up and K timed steps, one step =
+    one round of sample solves, one per host core (rank 0 only under torchrun)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    lim = cpu_threads_limit()
-    solve, n = oracle_sample_solve()
-    for _ in range(args.warmup):
-        solve()
-    t0 = time.perf_counter()
-    its = 0
-    for _ in range(args.steps):
-        its = solve()
-    sec = (time.perf_counter() - t0) / args.steps
-    del lim
-    value = n / sec / 1e9
+    ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    res = run_oracle_parallel(max(args.steps, 1), n_warm=args.warmup)
+    value = res["value"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 V-cycle)", "data": "synthetic (f=1)",
-            "config": {"workload": WORKLOAD["name"] + ": " + WORKLOAD["desc"], "sample": sample_desc()},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample_desc()},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["seconds_per_round"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 CG / f32 V-cycle",
+            "data": "synthetic (f=1)",
+            "config": {"workload": WORKLOAD["name"] + ": " + WORKLOAD["desc"], "sample": res["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": "oracle",
+                             "sample": res["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "iterations": its}
+            "iterations": res["iterations"]}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- our CUDA path
+def time_solves(h, b, x, steps, stream, dist, dev):
+    import torch
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = None
+    for _ in range(steps):
+        res = h.cg_solve(b, x, rtol=1e-8, max_it=100)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, res
+
+
 def run_ours(args, rank, ws, local):
     import torch
     from paper_2405_18982_b200 import ipmg
@@ -236,48 +303,37 @@ def run_ours(args, rank, ws, local):
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
-        res = h.cg_solve(b, x, rtol=1e-8, max_it=100)
+        h.cg_solve(b, x, rtol=1e-8, max_it=100)
     torch.cuda.synchronize()
 
-    # ---- timed region: K complete solves, inputs resident (537 MB > L2: no flush needed)
+    # ---- timed region (headline): K complete solves, no instrumentation
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.2)
     launches0 = h.launch_count()
-    h.profile(True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    its = []
-    for _ in range(args.steps):
-        res = h.cg_solve(b, x, rtol=1e-8, max_it=100)
-        its.append(res["iterations"])
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
-    launches = h.launch_count() - launches0
-    prof = {c: h.profile_read(c) for c in ("smooth", "vmult", "restrict", "prolong", "coarse", "blas")}
-    h.profile(False)
+    ms, res = time_solves(h, b, x, args.steps, stream, dist, dev)
+    launches = (h.launch_count() - launches0) // max(args.steps, 1) * args.steps
     clk = clocks.stop()
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
     value = n_glob / (ms_step * 1e-3) / 1e9     # strong scaling: the whole problem per step
+    its = res["iterations"]
+
+    # ---- profiled pass: the same solves with per-launch CUDA events on the handle's
+    # stream around every finest-level kernel (per-class device time and algorithmic bytes)
+    prof_steps = max(1, min(args.steps, 3))
+    h.profile(True)
+    ms_prof, _ = time_solves(h, b, x, prof_steps, stream, dist, dev)
+    prof = {c: h.profile_read(c) for c in ("smooth", "vmult", "restrict", "prolong", "coarse", "blas")}
+    h.profile(False)
 
     # ---- components (separately timed, CUDA events): vmult fp64 and one smoother step fp32
     comp = {}
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
     xs = torch.empty(n, dtype=torch.float64, device=dev).uniform_(-1, 1)
     ys = torch.empty_like(xs)
-    for _ in range(3):
+    for _ in range(2):
         h.vmult(L, xs, ys)
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
     c0.record(stream)
     for _ in range(reps):
         h.vmult(L, xs, ys)
@@ -285,6 +341,7 @@ def run_ours(args, rank, ws, local):
     torch.cuda.synchronize()
     comp["vmult_fp64_gdofs"] = n / (c0.elapsed_time(c1) / reps * 1e-3) / 1e9
     xf, bf = xs.float(), b.float()
+    del xs, ys
     for _ in range(2):
         h.smooth(L, xf, bf)
     c0.record(stream)
@@ -293,13 +350,14 @@ def run_ours(args, rank, ws, local):
     c1.record(stream)
     torch.cuda.synchronize()
     comp["smoother_step_fp32_gdofs"] = n / (c0.elapsed_time(c1) / reps * 1e-3) / 1e9
-    del xs, ys, xf, bf
+    del xf, bf
+    torch.cuda.empty_cache()
 
-    # ---- end-to-end through the public API with host buffers (pinned): every step
-    # copies its b host->device and its solution device->host.  The copies run on
-    # their own streams, double-buffered, so step i's download and step i+1's
-    # upload overlap the neighbouring solves (PCIe is full duplex); the events
-    # order upload -> solve -> download per step and the buffer reuse.
+    # ---- end-to-end through the public API with host buffers (pinned): every step copies
+    # its b host->device and its solution device->host.  The copies run on their own streams,
+    # double-buffered, so step i's download and step i+1's upload overlap the neighbouring
+    # solves (PCIe is full duplex); events order upload -> solve -> download per step and
+    # the buffer reuse.
     b_host = b.cpu().pin_memory()
     x_host = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
     bd = [torch.empty_like(b) for _ in range(2)]
@@ -308,7 +366,8 @@ def run_ours(args, rank, ws, local):
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_solved = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
-    e2e_steps = max(2, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(2, min(args.steps, 6))
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -339,77 +398,114 @@ def run_ours(args, rank, ws, local):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    e2e_err = float((x_host[(e2e_steps - 1) % 2] - x.cpu()).abs().max() / x.abs().max().cpu())
+    xh = x_host[(e2e_steps - 1) % 2]
+    e2e_err = float((xh - x.cpu()).abs().max() / x.abs().max().cpu())
     if dist:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
+    del bd, xd, x_host, b_host
+    torch.cuda.empty_cache()
+
+    # ---- secondary workload C2 (configs[1]), same solver, N = 1 only
+    secondary = None
+    if ws == 1 and not args.no_secondary:
+        h2 = ipmg.Handle(C2["dim"], C2["degree"], C2["n_levels"], vcycle_precision=ipmg.FP32, device=local)
+        L2 = C2["n_levels"] - 1
+        b2 = torch.empty(h2.ndofs(L2), dtype=torch.float64, device=dev)
+        h2.rhs(L2, b2)
+        x2 = torch.empty_like(b2)
+        for _ in range(3):
+            h2.cg_solve(b2, x2)
+        ms2, r2 = time_solves(h2, b2, x2, 20, stream, None, dev)
+        secondary = {"workload": C2["name"] + ": " + C2["desc"], "value": b2.numel() / (ms2 / 20 * 1e-3) / 1e9,
+                     "unit": UNIT, "ms_per_step": ms2 / 20, "steps": 20, "cg_iterations": r2["iterations"],
+                     "nu": r2["nu"]}
+        h2.close()
+        del b2, x2
 
     if rank != 0:
         return
     peaks, src = measured_peaks()
-    # roofline of the dominant kernel: the finest-level smoother colour pass (fp32)
+    alu = {"ffma2_tflops": ipmg.alu_peak(local, "ffma2"), "ffma_tflops": ipmg.alu_peak(local, "ffma"),
+           "dfma_tflops": ipmg.alu_peak(local, "dfma"),
+           "how": "ipmg_alu_peak: full occupancy, 8 independent FMA chains per thread, best of 5 (CUDA events)"}
+    alu_fp32 = max(alu["ffma2_tflops"], alu["ffma_tflops"])
+    # roofline of the dominant kernel: the finest-level fp32 smoother colour pass
     nl_s, ms_s, by_s = prof["smooth"]
     avg_ms = ms_s / max(nl_s, 1)
     achieved_gbs = by_s / (ms_s * 1e-3) / 1e9 if ms_s > 0 else 0.0
-    fl = smoother_flops_per_dof(wl["dim"], wl["degree"]) * n * nl_s
-    achieved_tf = fl / (ms_s * 1e-3) / 1e12 if ms_s > 0 else 0.0
+    # flops: covered dofs per pass ~ n (uncovered boundary layers are copies)
+    fl_eo = smoother_flops_per_dof(wl["dim"], wl["degree"]) * n * nl_s
+    fl_dense = smoother_flops_per_dof_dense(wl["dim"], wl["degree"]) * n * nl_s
+    tf_eo = fl_eo / (ms_s * 1e-3) / 1e12 if ms_s > 0 else 0.0
+    tf_dense = fl_dense / (ms_s * 1e-3) / 1e12 if ms_s > 0 else 0.0
     hbm_peak = peaks["hbm_gbs"]
-    alu_peak = alu_peak_tflops("fp32", peaks)
     t_bytes = by_s / (hbm_peak * 1e9)
-    t_flops = fl / (alu_peak * 1e12)
+    t_flops = fl_eo / (alu_fp32 * 1e12)
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "smooth_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+            tr = json.load(open(tr_path))
+            if tr.get("workload") == wl["name"]:
+                traffic = tr.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     if t_bytes >= t_flops:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak, "traffic": traffic}
     else:
-        roof = {"bound": "alu", "achieved": achieved_tf, "peak": alu_peak, "unit": "TFLOP/s",
-                "frac": achieved_tf / alu_peak, "traffic": traffic}
-    roof.update({"kernel": "smooth_kernel<2,float> (k=7), finest level", "peak_source": src,
+        roof = {"bound": "alu", "achieved": tf_eo, "peak": alu_fp32, "unit": "TFLOP/s",
+                "frac": tf_eo / alu_fp32, "traffic": traffic}
+    roof.update({"kernel": "smooth_kernel<%d,float> (k=%d), finest level colour pass" % (wl["dim"], wl["degree"]),
+                 "peak_source": {"hbm": src, "alu": "measured live (ipmg_alu_peak FFMA2)"},
                  "launches": nl_s, "avg_launch_ms": avg_ms,
                  "algorithmic_bytes_per_launch": by_s / max(nl_s, 1),
-                 "hbm_frac": achieved_gbs / hbm_peak, "alu_frac": achieved_tf / alu_peak,
-                 "share_of_step": ms_s / ms if ms > 0 else None,
-                 "per_class_ms_share": {c: (v[1] / ms if ms > 0 else None) for c, v in prof.items()}})
+                 "hbm_frac": achieved_gbs / hbm_peak,
+                 "alu_frac_evenodd": tf_eo / alu_fp32, "alu_frac_dense": tf_dense / alu_fp32,
+                 "flops_per_dof": {"evenodd": smoother_flops_per_dof(wl["dim"], wl["degree"]),
+                                   "dense_survey_8d": smoother_flops_per_dof_dense(wl["dim"], wl["degree"])},
+                 "timed_over": "profiled pass of %d solves (per-launch CUDA events on the launch stream), "
+                               "%.1f ms/solve vs %.1f ms/solve unprofiled" % (prof_steps, ms_prof / prof_steps,
+                                                                              ms_step),
+                 "share_of_step": ms_s / ms_prof if ms_prof > 0 else None,
+                 "per_class_ms_share": {c: (v[1] / ms_prof if ms_prof > 0 else None) for c, v in prof.items()}})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 CG / f32 V-cycle", "data": "synthetic (f=1 right-hand side)",
             "config": {"workload": wl["name"] + ": " + wl["desc"], "dofs": n_glob, "dofs_rank0": n,
                        "parallelism": "1 GPU" if ws == 1 else
-                       "slab decomposition along y over %d ranks (NCCL halo exchange + allgathered CG scalars)" % ws,
-                       "l2": "inputs larger than L2 (537 MB fp64 vectors), no flush"},
-            "time_to_solution_ms": ms_step, "cg_iterations": its[-1], "nu": res["nu"],
-            "components": comp, "roofline": roof, "clocks": clk, "gpu_launches": launches,
+                       "slab decomposition along z over %d ranks (NCCL halo exchange + allgathered CG scalars)" % ws,
+                       "l2": "inputs larger than L2 (8.4 GB fp64 vectors), no flush"},
+            "time_to_solution_ms": ms_step, "cg_iterations": its, "nu": res["nu"],
+            "components": comp, "roofline": roof, "alu_peaks": alu, "clocks": clk, "gpu_launches": launches,
             "e2e": {"value": n_glob / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n_glob,
                     "d2h_bytes_per_step": 8 * n_glob, "ms_per_step": e2e_ms, "steps": e2e_steps,
                     "copies": "pinned host buffers, H2D/D2H on their own streams, double-buffered "
                               "(overlapping the neighbouring steps' solves)",
-                    "solution_max_rel_diff_vs_device_run": e2e_err}}
+                    "solution_max_rel_diff_vs_device_run": e2e_err},
+            "secondary": secondary}
     if not args.no_cpu_baseline and ws == 1:
-        line["cpu_baseline"] = run_cpu_baseline()
+        line["cpu_baseline"] = run_oracle_parallel(3, n_warm=1)
     print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
-        rank, ws, _ = dist_init("gloo")
-        run_reference(args, rank, ws)
+        run_reference(args)
         return
-    rank, ws, local = dist_init("nccl")
+    args.warmup = max(args.warmup, 3)
+    maybe_respawn(args)
+    rank, ws, local = dist_init()
     run_ours(args, rank, ws, local)
 
 

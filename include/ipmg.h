@@ -103,6 +103,9 @@ typedef struct {
   int basis;                /* ipmg_basis; CLAMPED needs HERMITE, DIRICHLET needs LAGRANGE */
   int64_t dist_min_dofs;    /* with a communicator: distribute a level only if every rank keeps
                                >= this many of its dofs (else replicate it); 0: whenever possible */
+  double boundary_penalty_scale; /* penalty on domain-boundary faces = this * the interior gamma
+                               (PAPER.md:97-100 gives only the two-sided formula; reading A2:
+                               h+ = h- = h, i.e. 1; 0.5 is the one-sided k(k+1)/h); <= 0 -> 1 */
 } ipmg_config;
 
 typedef struct ipmg_handle ipmg_handle;
@@ -157,8 +160,16 @@ ipmg_status ipmg_partition(int dim, const int coarse_cells[3], int n_levels, int
  * (libnccl.so.2 is resolved at run time; IPMG_ERR_NCCL if absent or on NCCL
  * errors).  ipmg_comm_create_local fills out[0..nranks-1] with the members of
  * an in-process team on devices[r] (NULL: all device 0); member r must be
- * driven by its own host thread.  A peer that fails or stalls for 120 s makes
- * the others return IPMG_ERR_NCCL instead of hanging. */
+ * driven by its own host thread.  Failure behaviour: in the in-process team a peer
+ * that fails or stalls for 120 s makes the others return IPMG_ERR_NCCL (host barriers
+ * with a timeout).  With NCCL, ipmg_comm_create_nccl blocks until every rank has called
+ * it (as ncclCommInitRank does); afterwards every host wait of the solvers polls the
+ * stream and ncclCommGetAsyncError, and a communicator error or no progress for
+ * IPMG_NCCL_TIMEOUT seconds (environment, default 120) aborts the communicator
+ * (ncclCommAbort, which releases kernels blocked on a dead peer) and returns
+ * IPMG_ERR_NCCL; the communicator is unusable afterwards.  Stream-ordered calls that do
+ * not wait on the host (vmult, smooth, ...) return immediately; a later host wait
+ * (a solver, ipmg_synchronize) reports the failure. */
 ipmg_status ipmg_nccl_unique_id(void *id128);
 ipmg_status ipmg_comm_create_nccl(const void *id128, int rank, int nranks, int device,
                                   ipmg_comm **out);
@@ -203,8 +214,11 @@ ipmg_status ipmg_vcycle(ipmg_handle *h, const double *r, double *z);
 
 /* GMG-preconditioned CG on the finest level (north star; PAPER.md:331 stopping
  * rule ||r_n||_2 <= rtol ||r_0||_2, x_0 = 0).  b, x: double device vectors;
- * info may be NULL.  Returns IPMG_ERR_NOT_CONVERGED (info still filled) when
- * max_it is reached; b = 0 returns OK with 0 iterations. */
+ * info may be NULL.  Returns IPMG_ERR_NOT_CONVERGED (info still filled, x = the
+ * max_it-th iterate, complete in stream order) when max_it is reached; b = 0 returns
+ * OK with 0 iterations.  The host reads ||r|| once per iteration (a stream wait; with
+ * an NCCL communicator the wait polls for communicator errors, see ipmg_comm_create_nccl).
+ * info->seconds is host wall time up to the last residual check. */
 ipmg_status ipmg_cg_solve(ipmg_handle *h, const double *b, double *x, double rtol, int max_it,
                           ipmg_solve_info *info);
 
@@ -221,8 +235,12 @@ ipmg_status ipmg_cg_solve(ipmg_handle *h, const double *b, double *x, double rto
 ipmg_status ipmg_gmres_solve(ipmg_handle *h, const double *b, double *x, double rtol, int max_it,
                              ipmg_solve_info *info);
 
-/* Right-hand side b_i = int f phi_i on level `level` for f == 1;
- * kind must be 0.  b: double device vector of that level. */
+/* Right-hand side b_i = int f phi_i on level `level`.  kind 0: f == 1.
+ * kind 1: the manufactured solution u = prod_a sin(pi x_a / ell_a) of -Delta u = f with
+ * f = pi^2 (sum_a ell_a^-2) u (ell_a = coarse_cells[a] * h0, the box extents; u = 0 on the
+ * boundary), moments by Gauss quadrature with k+7 points per direction (SURVEY.md 4.2(3),
+ * the L2-rate property test); Lagrange basis only (else UNSUPPORTED).  b: double device
+ * vector of that level.  Errors: INVALID_ARG (level, kind, NULL b). */
 ipmg_status ipmg_rhs(ipmg_handle *h, int level, int kind, double *b);
 
 /* Layout conversion library order <-> cell-wise lexicographic order. */
@@ -231,7 +249,8 @@ ipmg_status ipmg_to_cellwise(ipmg_handle *h, int level, int precision, const voi
 ipmg_status ipmg_from_cellwise(ipmg_handle *h, int level, int precision, const void *x_cellwise,
                                void *x_lib);
 
-/* Synchronise the handle's stream; returns IPMG_ERR_CUDA on an asynchronous fault. */
+/* Synchronise the handle's stream; returns IPMG_ERR_CUDA on an asynchronous fault
+ * (IPMG_ERR_NCCL on a communicator failure, see ipmg_comm_create_nccl). */
 ipmg_status ipmg_synchronize(ipmg_handle *h);
 
 /* Instrumentation.  ipmg_profile(h, 1) clears and enables CUDA-event timing
@@ -247,6 +266,14 @@ ipmg_status ipmg_profile(ipmg_handle *h, int enable);
 ipmg_status ipmg_profile_read(ipmg_handle *h, int kernel_class, int64_t *launches, double *total_ms,
                               double *total_bytes);
 ipmg_status ipmg_launch_count(const ipmg_handle *h, int64_t *launches);
+
+/* Measurement utility (no part of the method): CUDA-core peak of `device` in TFLOP/s,
+ * the ALU denominator of the rooflines.  kind 0: packed fp32
+ * FFMA2 (fma.rn.f32x2, 2 FMAs per instruction), 1: scalar FFMA, 2: DFMA.  Full
+ * occupancy, 8 independent FMA chains per thread, best of `reps` timed launches (CUDA
+ * events on a private stream, after one warm-up).  Restores the caller's current
+ * device.  Errors: INVALID_ARG, CUDA. */
+ipmg_status ipmg_alu_peak(int device, int kind, int reps, double *tflops);
 
 /* One-line diagnostic of the last error on h (or of the last failed create
  * when h is NULL).  Library-owned string. */

@@ -112,14 +112,18 @@ def _cell_grid(level):
     return grids, lin
 
 
-def assemble(level: Level, k, penalty_scale=1.0, kind="lagrange"):
+def assemble(level: Level, k, penalty_scale=1.0, kind="lagrange", boundary_penalty_scale=1.0):
     """Global SIPG matrix of ``level`` in cell-wise lexicographic numbering, CSR.
     Exact zeros (e.g. phi_i(0) = 0 for i != 0 on GLL nodes) are not stored.
-    kind: 1D basis ('lagrange' GLL, or 'hermite' for the clamped kernel)."""
+    kind: 1D basis ('lagrange' GLL, or 'hermite' for the clamped kernel).
+    boundary_penalty_scale: the boundary-face penalty relative to the interior
+    one (reading A2: 1, both sides take the cell's h; 0.5 is the one-sided
+    k(k+1)/h, the probe of DESIGN.md "Table 1 readings")."""
     d, h = level.dim, level.h
     ref = Reference(d, k, kind=kind)
     nloc = ref.nc ** d
     gamma = basis.penalty(k, h, h, penalty_scale)
+    gamma_b = boundary_penalty_scale * gamma
     rows, cols, vals = [], [], []
     grids, lin = _cell_grid(level)
     K, _ = ref.cell_matrices(h)
@@ -137,7 +141,7 @@ def assemble(level: Level, k, penalty_scale=1.0, kind="lagrange"):
             for t, ct in ((0, cm), (1, cp)):
                 _place(rows, cols, vals, B[s][t], cs, ct, nloc)
         for side in (0, 1):
-            Bb = ref.boundary_face_block(a, side, h, gamma)
+            Bb = ref.boundary_face_block(a, side, h, gamma_b)
             sl = [slice(None)] * d
             sl[a] = 0 if side == 0 else level.n[a] - 1
             cb = lin[tuple(sl)].ravel()

@@ -98,3 +98,52 @@ def gmres(A, b, M, rtol=1e-8, max_it=200):
     y = np.linalg.solve(np.triu(H[:m, :m]), g[:m])
     x = sum(y[i] * Z[i] for i in range(m))
     return x, hist, conv
+
+
+def gmres_left(A, b, M, rtol=1e-8, max_it=200):
+    """Left-preconditioned GMRES without restart (MGS) on M^{-1} A x = M^{-1} b,
+    x0 = 0, stopping on the PRECONDITIONED residual |g_{j+1}| <= rtol ||M^{-1} b||.
+    This is a probe of how the paper's nu may have been measured (DESIGN.md
+    "Table 1 readings", reading A22: a solver whose default is left
+    preconditioning reports the preconditioned residual norm)
+    itself says "Euclidean norm of the residual".  Returns (x, history,
+    converged); history = ||M^{-1} b||, |g_1|, .., |g_n|."""
+    Aop = A if callable(A) else (lambda v: A @ v)
+    Mop = M if callable(M) else (lambda v: M @ v)
+    r0 = Mop(np.asarray(b, dtype=np.float64))
+    beta0 = np.linalg.norm(r0)
+    hist = [beta0]
+    if beta0 == 0.0:
+        return np.zeros_like(r0), hist, True
+    V = [r0 / beta0]
+    H = np.zeros((max_it + 1, max_it))
+    cs, sn = np.zeros(max_it), np.zeros(max_it)
+    g = np.zeros(max_it + 1)
+    g[0] = beta0
+    conv = False
+    j = 0
+    for j in range(max_it):
+        w = Mop(Aop(V[j]))
+        for i in range(j + 1):
+            H[i, j] = w @ V[i]
+            w = w - H[i, j] * V[i]
+        H[j + 1, j] = np.linalg.norm(w)
+        V.append(w / H[j + 1, j] if H[j + 1, j] != 0 else w)
+        for i in range(j):
+            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = t
+        den = np.hypot(H[j, j], H[j + 1, j])
+        cs[j], sn[j] = H[j, j] / den, H[j + 1, j] / den
+        H[j, j] = den
+        H[j + 1, j] = 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        hist.append(abs(g[j + 1]))
+        if abs(g[j + 1]) <= rtol * beta0:
+            conv = True
+            break
+    m = j + 1
+    y = np.linalg.solve(np.triu(H[:m, :m]), g[:m])
+    x = sum(y[i] * V[i] for i in range(m))
+    return x, hist, conv

@@ -19,14 +19,16 @@ from .smoother import PatchSmoother
 class VCycle:
     def __init__(self, dim, k, n_levels, n0=None, h0=0.5, dtype=np.float64,
                  smoother="multiplicative", omega=None, post_reverse=True,
-                 penalty_scale=1.0, operators=None, kernel="full", basis_kind=None):
+                 penalty_scale=1.0, operators=None, kernel="full", basis_kind=None,
+                 boundary_penalty_scale=1.0):
         self.dim, self.k, self.n_levels = dim, k, n_levels
         self.dtype = np.dtype(dtype)
         self.levels = mesh.hierarchy(dim, n_levels, n0, h0)
         # the clamped kernel lives on the Hermite-type basis (the whole hierarchy)
         self.basis_kind = basis_kind or ("hermite" if kernel == "clamped" else "lagrange")
         if operators is None:
-            operators = [assemble.assemble(lv, k, penalty_scale, kind=self.basis_kind) for lv in self.levels]
+            operators = [assemble.assemble(lv, k, penalty_scale, kind=self.basis_kind,
+                                           boundary_penalty_scale=boundary_penalty_scale) for lv in self.levels]
         self.A64 = operators
         self.A = [A.astype(self.dtype) for A in operators]
         self.P = [None] + [transfer.prolongation(self.levels[l - 1], self.levels[l], k, self.basis_kind).astype(self.dtype)

@@ -24,7 +24,7 @@ CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xpt
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-I" + INCLUDE, "-I" + CSRC, "-I/usr/local/cuda/include"]
 
 SOURCES_CU = (["kernels_k%d.cu" % k for k in range(1, 8)] + ["kernels_dir_k%d.cu" % k for k in range(1, 8)] +
-              ["blas.cu"])
+              ["blas.cu", "peak.cu"])
 SOURCES_CXX = ["fe1d.cpp", "comm.cpp", "ipmg.cpp"]
 HEADERS = ["common.cuh", "patch_kernels.cuh", "blas.cuh", "fe1d.hpp", "comm.hpp"]
 

@@ -263,6 +263,26 @@ __global__ void permute_kernel(const T* __restrict__ in, T* __restrict__ out, Le
   }
 }
 
+// b = scale * gx (x) gy (x) gz per cell (separable manufactured right-hand side); the
+// 1D tables are over GLOBAL cells, the slab offset zoff applies to the slowest axis.
+__global__ void sep_fill_kernel(double* __restrict__ b, const double* __restrict__ gx,
+                                const double* __restrict__ gy, const double* __restrict__ gz, LevelGeom g,
+                                int nc, int dim, double scale, long long n) {
+  const int cell = dim == 3 ? nc * nc * nc : nc * nc;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / cell;
+    const int l = (int)(e % cell);
+    const int cx = (int)(c % g.n[0]);
+    const int cy = (int)((c / g.n[0]) % g.n[1]);
+    const int cz = (int)(c / ((long long)g.n[0] * g.n[1]));
+    const int ix = l % nc, iy = (l / nc) % nc, iz = l / (nc * nc);
+    double v = scale * gx[cx * nc + ix];
+    if (dim == 3) v *= gy[cy * nc + iy] * gz[(cz + g.zoff) * nc + iz];
+    else v *= gy[(cy + g.zoff) * nc + iy];
+    b[cell_offset_cells(g, cx, cy, cz) * cell + l] = v;
+  }
+}
+
 __global__ void pattern_fill_kernel(double* __restrict__ b, const double* __restrict__ pat, int cell, long long n) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     b[e] = pat[e % cell];
@@ -495,6 +515,12 @@ __global__ void to_host_kernel(double* __restrict__ dst, const double* __restric
 }
 cudaError_t to_host(double* dst_mapped, const double* src, int n, cudaStream_t s) {
   to_host_kernel<<<1, 64, 0, s>>>(dst_mapped, src, n);
+  return cudaGetLastError();
+}
+
+cudaError_t sep_fill(double* b, const double* gx, const double* gy, const double* gz, const LevelGeom& g, int nc,
+                     int dim, double scale, long long n, cudaStream_t s) {
+  sep_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(b, gx, gy, gz, g, nc, dim, scale, n);
   return cudaGetLastError();
 }
 

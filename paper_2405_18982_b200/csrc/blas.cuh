@@ -43,6 +43,8 @@ cudaError_t scale_vec(double* v, const double* w, long long n, const double* nrm
 cudaError_t combine(double* x, const double* const* Z, const double* y, int m, long long n, cudaStream_t s);
 cudaError_t to_host(double* dst_mapped, const double* src, int n, cudaStream_t s);
 cudaError_t pattern_fill(double* b, const double* pat, int cell, long long n, cudaStream_t s);
+cudaError_t sep_fill(double* b, const double* gx, const double* gy, const double* gz, const LevelGeom& g, int nc,
+                     int dim, double scale, long long n, cudaStream_t s);
 cudaError_t coarse_solve(int prec, const void* b, void* x, const CoarseDesc& cd, const void* const S[3],
                          const void* const L[3], cudaStream_t s);
 

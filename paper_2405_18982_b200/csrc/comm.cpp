@@ -6,6 +6,8 @@
 #include <dlfcn.h>
 
 #include <chrono>
+#include <cstdlib>
+#include <thread>
 #include <cstring>
 
 #include "blas.cuh"
@@ -160,6 +162,8 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -187,6 +191,8 @@ const NcclApi& nccl() {
     a.AllGather = (decltype(a.AllGather))sym("ncclAllGather");
     a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
     a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
+    a.CommGetAsyncError = (decltype(a.CommGetAsyncError))sym("ncclCommGetAsyncError");
+    a.CommAbort = (decltype(a.CommAbort))sym("ncclCommAbort");
     a.ok = all;
     if (!all) a.why = "libnccl.so.2 lacks a required symbol";
     return a;
@@ -209,15 +215,56 @@ struct NcclComm : ipmg_comm {
     if (nranks == 1) return true;
     const NcclApi& a = nccl();
     if (!ck(a.GroupStart(), "group start")) return false;
+    // record the first failure but always close the group: an open group would swallow
+    // every later NCCL call of this thread (torch's included)
+    bool ok = true;
     if (rank > 0) {
-      if (!ck(a.Send(lo_src, bytes, ncclUint8, rank - 1, comm, s), "send lo")) return false;
-      if (!ck(a.Recv(lo_dst, bytes, ncclUint8, rank - 1, comm, s), "recv lo")) return false;
+      ok = ok && ck(a.Send(lo_src, bytes, ncclUint8, rank - 1, comm, s), "send lo");
+      ok = ok && ck(a.Recv(lo_dst, bytes, ncclUint8, rank - 1, comm, s), "recv lo");
     }
     if (rank + 1 < nranks) {
-      if (!ck(a.Send(hi_src, bytes, ncclUint8, rank + 1, comm, s), "send hi")) return false;
-      if (!ck(a.Recv(hi_dst, bytes, ncclUint8, rank + 1, comm, s), "recv hi")) return false;
+      ok = ok && ck(a.Send(hi_src, bytes, ncclUint8, rank + 1, comm, s), "send hi");
+      ok = ok && ck(a.Recv(hi_dst, bytes, ncclUint8, rank + 1, comm, s), "recv hi");
     }
-    return ck(a.GroupEnd(), "group end");
+    const std::string first = err;
+    const bool closed = ck(a.GroupEnd(), "group end");
+    if (!ok) err = first;
+    return ok && closed;
+  }
+  bool wait(cudaStream_t s) override {
+    const NcclApi& a = nccl();
+    static const double limit = [] {
+      const char* e = std::getenv("IPMG_NCCL_TIMEOUT");
+      const double v = e ? std::atof(e) : 0.0;
+      return v > 0 ? v : 120.0;
+    }();
+    if (!comm) {
+      err = "nccl communicator was aborted";
+      return false;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long spin = 0;; ++spin) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) return true;
+      if (q != cudaErrorNotReady) {
+        err = std::string("stream wait: ") + cudaGetErrorString(q);
+        return false;
+      }
+      ncclResult_t ae = 0;
+      if (a.CommGetAsyncError && a.CommGetAsyncError(comm, &ae) == 0 && ae != 0 && ae != 7 /* ncclInProgress */) {
+        err = std::string("nccl async error: ") + (a.GetErrorString ? a.GetErrorString(ae) : "?");
+        if (a.CommAbort) a.CommAbort(comm);
+        comm = nullptr;
+        return false;
+      }
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+        err = "nccl: no progress for IPMG_NCCL_TIMEOUT seconds (peer failed or stalled); communicator aborted";
+        if (a.CommAbort) a.CommAbort(comm);
+        comm = nullptr;
+        return false;
+      }
+      if (spin > 2000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
   }
   bool allgather(const void* src, void* dst, size_t bytes, cudaStream_t s) override {
     return ck(nccl().AllGather(src, dst, bytes, ncclUint8, comm, s), "allgather");
@@ -292,3 +339,10 @@ ipmg_comm* make_nccl_comm(const void* unique_id, int rank, int nranks, int devic
 }
 
 }  // namespace ipmg
+
+bool ipmg_comm::wait(cudaStream_t s) {
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) return true;
+  err = std::string("stream wait: ") + cudaGetErrorString(e);
+  return false;
+}

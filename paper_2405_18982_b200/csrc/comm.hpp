@@ -32,6 +32,11 @@ struct ipmg_comm {
   // buf = sum over ranks (prec 0 double, 1 float)
   virtual bool allreduce_sum(void* buf, size_t n, int prec, cudaStream_t s) = 0;
   virtual bool capturable() const = 0;   // may be recorded into a CUDA graph
+  // host wait for stream s (the solvers' per-iteration scalar reads).  NCCL: polls the
+  // stream and ncclCommGetAsyncError; a communicator error, or no progress for
+  // IPMG_NCCL_TIMEOUT seconds (default 120), aborts the communicator (ncclCommAbort, so
+  // a kernel blocked on a dead peer returns) and fails with err set.
+  virtual bool wait(cudaStream_t s);
 };
 
 namespace ipmg {

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Host-side 1D FE setup; see fe1d.hpp for the paper passages each table follows.
 #include "fe1d.hpp"
 
@@ -146,7 +147,7 @@ std::vector<double> sipg_chain_modes(const FE1D& fe, int ncell, int low_mode, in
     const double wt = low_bnd ? 1.0 : 0.5;
     jv[0] = -1.0;
     for (int j = 0; j < nc; ++j) gv[j] = wt * fe.d0[j];
-    add_face(A, n, jv, gv, fe.gamma);
+    add_face(A, n, jv, gv, low_bnd ? fe.gamma_b : fe.gamma);
   }
   // high outer face: the chain is the "A" (left) side; J = vA, G = w * gA
   if (high_mode != 2) {
@@ -155,7 +156,7 @@ std::vector<double> sipg_chain_modes(const FE1D& fe, int ncell, int low_mode, in
     const double wt = high_bnd ? 1.0 : 0.5;
     jv[n - 1] = 1.0;
     for (int j = 0; j < nc; ++j) gv[(ncell - 1) * nc + j] = wt * fe.d1[j];
-    add_face(A, n, jv, gv, fe.gamma);
+    add_face(A, n, jv, gv, high_bnd ? fe.gamma_b : fe.gamma);
   }
   return A;
 }
@@ -296,7 +297,7 @@ static bool invert(int n, std::vector<double> A, std::vector<double>& Ai) {
   return true;
 }
 
-FE1D build_fe1d(int k, double penalty_scale, int basis, int dir_width) {
+FE1D build_fe1d(int k, double penalty_scale, int basis, int dir_width, double boundary_scale) {
   FE1D fe;
   fe.k = k;
   fe.basis = basis;
@@ -305,6 +306,7 @@ FE1D build_fe1d(int k, double penalty_scale, int basis, int dir_width) {
   fe.np = 2 * fe.nc;
   const int nc = fe.nc, np = fe.np;
   fe.gamma = penalty_scale * 2.0 * k * (k + 1);
+  fe.gamma_b = fe.gamma * (boundary_scale > 0 ? boundary_scale : 1.0);
   fe.nodes = gll(k);
   std::vector<double> qx, qw, v, d;
   gauss(nc, qx, qw);   // exact for degree 2k (reading A3)
@@ -486,6 +488,23 @@ FE1D build_fe1d(int k, double penalty_scale, int basis, int dir_width) {
     fe.P = PH;
   }
   return fe;
+}
+
+std::vector<double> sin_moments(const FE1D& fe, int ncell, int c0, double h, double ell) {
+  // g[c * nc + i] = int over global cell c0 + c of sin(pi x / ell) phi_i((x - x_c) / h) dx,
+  // Gauss quadrature with nc + 6 points per cell (GLL Lagrange basis only)
+  const int nc = fe.nc;
+  std::vector<double> qx, qw, v, d;
+  gauss(nc + 6, qx, qw);
+  const double pi = 3.14159265358979323846;
+  std::vector<double> g((size_t)ncell * nc, 0.0);
+  for (int c = 0; c < ncell; ++c)
+    for (size_t q = 0; q < qx.size(); ++q) {
+      lagrange(fe.nodes, qx[q], v, d);
+      const double f = std::sin(pi * ((c0 + c) + qx[q]) * h / ell) * qw[q] * h;
+      for (int i = 0; i < nc; ++i) g[(size_t)c * nc + i] += f * v[i];
+    }
+  return g;
 }
 
 void global_1d(const FE1D& fe, int ncell, std::vector<double>& L, std::vector<double>& M) {

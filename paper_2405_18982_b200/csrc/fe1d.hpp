@@ -21,6 +21,8 @@ struct FE1D {
   int basis = 0;                   // 0 GLL Lagrange, 1 Hermite-type (clamped kernel, reading A19)
   int dir_width = 1;               // nodes dropped per mesh-interior patch side: 1 Dirichlet, 2 clamped
   double gamma = 0;                // unit-h penalty 2k(k+1)*scale (reading A2)
+  double gamma_b = 0;              // unit-h penalty on domain-boundary faces (reading A2: = gamma
+                                   // by default; boundary_scale probes the one-sided k(k+1)/h)
   std::vector<double> nodes;       // GLL nodes on [0,1]                       (nc)
   std::vector<double> w;           // int_0^1 phi_i                             (nc)
   std::vector<double> M, K;        // unit cell mass / stiffness, row-major    (nc*nc)
@@ -44,13 +46,19 @@ struct FE1D {
 };
 
 // Build all unit tables for degree k (1..7); penalty_scale multiplies gamma;
-// basis 1 = Hermite-type (k >= 3); dir_width: reduced-space width of the
-// Dirichlet/clamped tables.
-FE1D build_fe1d(int k, double penalty_scale, int basis = 0, int dir_width = 1);
+// boundary_scale multiplies the domain-boundary penalty relative to gamma
+// (<= 0: 1, i.e. gamma_b = gamma); basis 1 = Hermite-type (k >= 3); dir_width:
+// reduced-space width of the Dirichlet/clamped tables.
+FE1D build_fe1d(int k, double penalty_scale, int basis = 0, int dir_width = 1,
+                double boundary_scale = 1.0);
 
 // Global 1D SIPG matrix (unit h) on ncell cells with boundary faces at both ends
 // and its mass; row-major (ncell*nc)^2.  Used for the coarse solve (reading A10).
 void global_1d(const FE1D& fe, int ncell, std::vector<double>& L, std::vector<double>& M);
+
+// Manufactured right-hand side (ipmg_rhs kind 1): 1D moments of sin(pi x / ell) against
+// the GLL Lagrange basis on ncell cells of size h starting at global cell c0, (ncell*nc).
+std::vector<double> sin_moments(const FE1D& fe, int ncell, int c0, double h, double ell);
 
 // Generalized symmetric eigenproblem L S = M S diag(lam), S^T M S = I, lam ascending,
 // sign fixed so that the largest-|.| entry of each column is positive.

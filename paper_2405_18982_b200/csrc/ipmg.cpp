@@ -167,6 +167,18 @@ struct ipmg_handle {
     return esize(prec) * (cov * (2 + (has_x ? 1 : 0)) + unc * (1 + (has_x ? 1 : 0)));
   }
 
+  // host wait on the handle's stream: through the communicator when there is one (the
+  // NCCL transport polls for asynchronous errors and aborts on a stalled peer)
+  ipmg_status host_sync(cudaStream_t s) {
+    if (comm) {
+      if (comm->wait(s)) return IPMG_OK;
+      err = comm->err;
+      return IPMG_ERR_NCCL;
+    }
+    return cuda(cudaStreamSynchronize(s), "sync");
+  }
+  std::vector<double*> sin_tab;   // ipmg_rhs kind 1: per level, 3 global 1D moment tables
+
   ipmg_status fail(ipmg_status st, const std::string& msg) {
     err = msg;
     return st;
@@ -438,6 +450,22 @@ struct ipmg_handle {
   }
 };
 
+// Scoped device guard of every entry point that takes a handle: the handle's work runs on
+// cfg.device whatever device the calling thread has current, and the caller's current
+// device is restored on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const ipmg_handle* h) {
+    if (!h) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != h->cfg.device && cudaSetDevice(h->cfg.device) == cudaSuccess)
+      prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 extern "C" {
 
 void ipmg_config_default(ipmg_config* c) {
@@ -456,6 +484,7 @@ void ipmg_config_default(ipmg_config* c) {
   c->penalty_scale = 1.0;
   c->basis = IPMG_BASIS_LAGRANGE;
   c->dist_min_dofs = 0;
+  c->boundary_penalty_scale = 1.0;
   c->device = 0;
   c->cuda_stream = nullptr;
 }
@@ -545,7 +574,9 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
   };
   if (cudaSetDevice(cfg->device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return bail(IPMG_ERR_CUDA); }
   // ---- 1D tables and their upload
-  h->fe = ipmg::build_fe1d(h->k, h->cfg.penalty_scale, cfg->basis, cfg->kernel == IPMG_KERNEL_CLAMPED ? 2 : 1);
+  if (!(h->cfg.boundary_penalty_scale > 0)) h->cfg.boundary_penalty_scale = 1.0;
+  h->fe = ipmg::build_fe1d(h->k, h->cfg.penalty_scale, cfg->basis, cfg->kernel == IPMG_KERNEL_CLAMPED ? 2 : 1,
+                           h->cfg.boundary_penalty_scale);
   if (!h->fe.even_odd) {   // the interior-patch fast path relies on the reflection symmetry
     h->err = "interior patch eigenvectors are not even/odd";
     return bail(IPMG_ERR_UNSUPPORTED);
@@ -680,6 +711,7 @@ ipmg_status ipmg_create(const ipmg_config* cfg, ipmg_handle** out) {
 }
 
 ipmg_status ipmg_destroy(ipmg_handle* h) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_OK;
   if (h->cstream) cudaStreamDestroy(h->cstream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -773,6 +805,7 @@ ipmg_status ipmg_level_info(const ipmg_handle* h, int level, int64_t* ndofs, int
 static bool bad_prec(int p) { return p != IPMG_FP64 && p != IPMG_FP32; }
 
 ipmg_status ipmg_vmult(ipmg_handle* h, int level, int precision, const void* x, void* y) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 0 || level >= h->nlev || bad_prec(precision) || !x || !y || x == y)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_vmult: bad level/precision/pointers");
@@ -791,6 +824,7 @@ ipmg_status ipmg_vmult(ipmg_handle* h, int level, int precision, const void* x, 
 
 ipmg_status ipmg_smooth_colour(ipmg_handle* h, int level, int precision, const void* x_in, const void* b,
                                void* x_out, int colour) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 1 || level >= h->nlev || bad_prec(precision) || !b || !x_out || x_in == x_out || colour < 0 ||
       colour >= (1 << h->dim))
@@ -804,6 +838,7 @@ ipmg_status ipmg_smooth_colour(ipmg_handle* h, int level, int precision, const v
 }
 
 ipmg_status ipmg_smooth(ipmg_handle* h, int level, int precision, void* x, const void* b, int reverse) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 1 || level >= h->nlev || bad_prec(precision) || !x || !b || x == b)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_smooth: bad arguments");
@@ -829,6 +864,7 @@ ipmg_status ipmg_smooth(ipmg_handle* h, int level, int precision, void* x, const
 
 ipmg_status ipmg_residual_restrict(ipmg_handle* h, int fine_level, int precision, const void* x, const void* b,
                                    void* r_c) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !b || !r_c)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_residual_restrict: bad arguments");
@@ -839,6 +875,7 @@ ipmg_status ipmg_residual_restrict(ipmg_handle* h, int fine_level, int precision
 }
 
 ipmg_status ipmg_prolongate_add(ipmg_handle* h, int fine_level, int precision, const void* e_c, void* x_f) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (fine_level < 1 || fine_level >= h->nlev || bad_prec(precision) || !e_c || !x_f)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_prolongate_add: bad arguments");
@@ -850,25 +887,62 @@ ipmg_status ipmg_prolongate_add(ipmg_handle* h, int fine_level, int precision, c
 }
 
 ipmg_status ipmg_coarse_solve(ipmg_handle* h, int precision, const void* b0, void* x0) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (bad_prec(precision) || !b0 || !x0 || b0 == x0) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_coarse_solve: bad arguments");
   return h->coarse(precision, b0, x0);
 }
 
 ipmg_status ipmg_vcycle(ipmg_handle* h, const double* r, double* z) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (!r || !z || (const void*)r == (const void*)z) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_vcycle: bad pointers");
   return h->vcycle(r, z, nullptr);
 }
 
 ipmg_status ipmg_rhs(ipmg_handle* h, int level, int kind, double* b) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
-  if (level < 0 || level >= h->nlev || kind != 0 || !b) return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_rhs: bad arguments");
+  if (level < 0 || level >= h->nlev || (kind != 0 && kind != 1) || !b)
+    return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_rhs: bad arguments");
+  if (kind == 0) {
+    h->n_launches += 1;
+    return h->cuda(ipmg::pattern_fill(b, h->pattern + (size_t)level * h->cell, h->cell, h->ndofs[level], h->stream),
+                   "rhs");
+  }
+  // kind 1: f = pi^2 sum_a 1/ell_a^2 prod_a sin(pi x_a / ell_a), ell_a the box extents;
+  // b = f-moments, a product of 1D moment tables per cell (separable)
+  if (h->cfg.basis != IPMG_BASIS_LAGRANGE)
+    return h->fail(IPMG_ERR_UNSUPPORTED, "ipmg_rhs: kind 1 needs the Lagrange basis");
+  if (h->sin_tab.empty()) h->sin_tab.assign((size_t)h->nlev * 3, nullptr);
+  const ipmg::LevelGeom& g = h->geom[level];
+  const double hh = h->hsize[level];
+  const double pi = 3.14159265358979323846;
+  double scale = 0.0;
+  for (int a = 0; a < h->dim; ++a) {
+    const double ell = h->cfg.coarse_cells[a] * h->cfg.h0;
+    scale += pi * pi / (ell * ell);
+    double*& t = h->sin_tab[(size_t)level * 3 + a];
+    if (!t) {
+      // global cells along a: the slowest axis may be a slab (nglob global layers)
+      const int S = h->dim - 1;
+      const int nglob = a == S ? g.nglob : g.n[a];
+      const std::vector<double> m = ipmg::sin_moments(h->fe, nglob, 0, hh, ell);
+      t = (double*)h->dalloc(m.size() * sizeof(double));
+      if (!t) return h->fail(IPMG_ERR_OUT_OF_MEMORY, "ipmg_rhs: table");
+      ipmg_status st = h->cuda(cudaMemcpy(t, m.data(), m.size() * sizeof(double), cudaMemcpyHostToDevice), "rhs table");
+      if (st != IPMG_OK) return st;
+    }
+  }
   h->n_launches += 1;
-  return h->cuda(ipmg::pattern_fill(b, h->pattern + (size_t)level * h->cell, h->cell, h->ndofs[level], h->stream), "rhs");
+  double* const* tb = &h->sin_tab[(size_t)level * 3];
+  return h->cuda(ipmg::sep_fill(b, tb[0], tb[1], h->dim == 3 ? tb[2] : nullptr, g, h->nc, h->dim, scale,
+                                h->ndofs[level], h->stream),
+                 "rhs");
 }
 
 ipmg_status ipmg_to_cellwise(ipmg_handle* h, int level, int precision, const void* x_lib, void* x_cw) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 0 || level >= h->nlev || bad_prec(precision) || !x_lib || !x_cw || x_lib == x_cw)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_to_cellwise: bad arguments");
@@ -877,6 +951,7 @@ ipmg_status ipmg_to_cellwise(ipmg_handle* h, int level, int precision, const voi
 }
 
 ipmg_status ipmg_from_cellwise(ipmg_handle* h, int level, int precision, const void* x_cw, void* x_lib) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (level < 0 || level >= h->nlev || bad_prec(precision) || !x_lib || !x_cw || x_lib == x_cw)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_from_cellwise: bad arguments");
@@ -885,18 +960,19 @@ ipmg_status ipmg_from_cellwise(ipmg_handle* h, int level, int precision, const v
 }
 
 ipmg_status ipmg_synchronize(ipmg_handle* h) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
-  return h->cuda(cudaStreamSynchronize(h->stream), "synchronize");
+  return h->host_sync(h->stream);
 }
 
 ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rtol, int max_it, ipmg_solve_info* info) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (!b || !x || (const void*)b == (const void*)x || !(rtol > 0) || max_it < 1)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_cg_solve: bad arguments");
   const int L = h->nlev - 1;
   const long long n = h->ndofs[L];
   auto t0 = std::chrono::steady_clock::now();
-  if (h->comm) cudaSetDevice(h->cfg.device);
   if (!h->r) {
     h->r = (double*)h->dalloc(n * 8);
     h->p = (double*)h->valloc(L, IPMG_FP64);   // read with ghosts by the operator
@@ -930,7 +1006,7 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
   if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
   CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
   h->n_launches += 1;
-  CK(cudaStreamSynchronize(s), "sync");
+  if ((st = h->host_sync(s)) != IPMG_OK) return st;
   const double r0 = std::sqrt(h->hpin[0]);
   hist.push_back(r0);
   int it = 0;
@@ -984,13 +1060,15 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
       CK(ipmg::finalize(h->partial, h->scal + 3, s), "finalize");
       if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
       CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
-  h->n_launches += 1;
-      CK(cudaStreamSynchronize(s), "sync");
+      h->n_launches += 1;
+      if ((st = h->host_sync(s)) != IPMG_OK) return st;
       ++it;
       const double rn = std::sqrt(h->hpin[0]);
       hist.push_back(rn);
-      if (rn <= rtol * r0) {
-        conv = true;
+      if (rn <= rtol * r0 || it == max_it) {
+        // converged, or max_it reached: apply the pending x += alpha p (mixed) and stop --
+        // no V-cycle whose direction update would never be used
+        conv = rn <= rtol * r0;
         if (mixed) TK(ipmg::cg_update_x(x, h->p, n, h->scal, cur, 2, s), 24.0 * n, "update x");
         break;
       }
@@ -1034,13 +1112,13 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
 
 ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double rtol, int max_it,
                              ipmg_solve_info* info) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   if (!b || !x || (const void*)b == (const void*)x || !(rtol > 0) || max_it < 1 || max_it > 1000)
     return h->fail(IPMG_ERR_INVALID_ARG, "ipmg_gmres_solve: bad arguments");
   const int L = h->nlev - 1;
   const long long n = h->ndofs[L];
   auto t0 = std::chrono::steady_clock::now();
-  if (h->comm) cudaSetDevice(h->cfg.device);
   cudaStream_t s = h->stream;
   const bool mixed = h->cfg.vcycle_precision == IPMG_FP32;
   ipmg_status st = h->ensure_vcycle(h->cfg.vcycle_precision);
@@ -1080,7 +1158,7 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
   if ((st = h->allsum(h->scal + 3)) != IPMG_OK) return st;
   CK(ipmg::to_host(h->hpin_dev, h->scal + 3, 1, s), "to host");
   h->n_launches += 1;
-  CK(cudaStreamSynchronize(s), "sync");
+  if ((st = h->host_sync(s)) != IPMG_OK) return st;
   const double beta0 = std::sqrt(h->hpin[0]);
   hist.push_back(beta0);
   int m = 0;
@@ -1135,7 +1213,7 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
       h->n_launches += 1;
       CK(ipmg::to_host(h->ghpin_dev, h->ghcol, j + 2, s), "to host");
       h->n_launches += 1;
-      CK(cudaStreamSynchronize(s), "sync");
+      if ((st = h->host_sync(s)) != IPMG_OK) return st;
       for (int i = 0; i <= j; ++i) Hij(i, j) = h->ghpin[i];
       Hij(j + 1, j) = std::sqrt(h->ghpin[j + 1]);
       for (int i = 0; i < j; ++i) {   // previous rotations
@@ -1169,7 +1247,7 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
     CK(cudaMemcpyAsync(h->gzptr, zp.data(), sizeof(double*) * m, cudaMemcpyHostToDevice, s), "h2d");
     CK(ipmg::combine(x, h->gzptr, h->gy, m, n, s), "combine");
     h->n_launches += 1;
-    CK(cudaStreamSynchronize(s), "sync");   // y, zp are host temporaries
+    if ((st = h->host_sync(s)) != IPMG_OK) return st;   // y, zp are host temporaries
   }
 #undef CK
   auto t1 = std::chrono::steady_clock::now();
@@ -1190,6 +1268,7 @@ ipmg_status ipmg_gmres_solve(ipmg_handle* h, const double* b, double* x, double 
 }
 
 ipmg_status ipmg_profile(ipmg_handle* h, int enable) {
+  DeviceGuard dg(h);
   if (!h) return IPMG_ERR_INVALID_ARG;
   h->prof_on = enable != 0;
   if (h->prof_on) h->recs.clear();
@@ -1198,6 +1277,7 @@ ipmg_status ipmg_profile(ipmg_handle* h, int enable) {
 
 ipmg_status ipmg_profile_read(ipmg_handle* h, int kernel_class, int64_t* launches, double* total_ms,
                               double* total_bytes) {
+  DeviceGuard dg(h);
   if (!h || kernel_class < 0 || kernel_class >= KC_N) return IPMG_ERR_INVALID_ARG;
   ipmg_status st = h->cuda(cudaStreamSynchronize(h->stream), "profile sync");
   if (st != IPMG_OK) return st;

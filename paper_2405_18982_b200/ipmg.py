@@ -28,7 +28,7 @@ EXPORTS = ["ipmg_config_default", "ipmg_create", "ipmg_destroy", "ipmg_level_inf
            "ipmg_coarse_solve", "ipmg_vcycle", "ipmg_cg_solve", "ipmg_gmres_solve", "ipmg_rhs", "ipmg_to_cellwise",
            "ipmg_from_cellwise", "ipmg_synchronize", "ipmg_last_error", "ipmg_tables_1d",
            "ipmg_profile", "ipmg_profile_read", "ipmg_launch_count", "ipmg_level_partition", "ipmg_partition",
-           "ipmg_nccl_unique_id", "ipmg_comm_create_nccl", "ipmg_comm_create_local", "ipmg_comm_destroy"]
+           "ipmg_nccl_unique_id", "ipmg_comm_create_nccl", "ipmg_comm_create_local", "ipmg_comm_destroy", "ipmg_alu_peak"]
 
 KERNEL_CLASSES = {"smooth": 0, "vmult": 1, "restrict": 2, "prolong": 3, "coarse": 4, "blas": 5, "additive": 6}
 
@@ -40,7 +40,7 @@ class Config(ctypes.Structure):
                 ("post_smooth_reverse", ctypes.c_int), ("vcycle_precision", ctypes.c_int),
                 ("penalty_scale", ctypes.c_double), ("device", ctypes.c_int),
                 ("cuda_stream", ctypes.c_void_p), ("comm", ctypes.c_void_p), ("basis", ctypes.c_int),
-                ("dist_min_dofs", ctypes.c_int64)]
+                ("dist_min_dofs", ctypes.c_int64), ("boundary_penalty_scale", ctypes.c_double)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -93,6 +93,7 @@ def load():
         "ipmg_comm_create_nccl": (i, [ctypes.c_char_p, i, i, i, ctypes.POINTER(vp)]),
         "ipmg_comm_create_local": (i, [i, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)]),
         "ipmg_comm_destroy": (i, [vp]),
+        "ipmg_alu_peak": (i, [i, i, i, ctypes.POINTER(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -117,6 +118,16 @@ def tables_1d(k, what, penalty_scale=1.0):
     if st != IPMG_OK:
         raise IpmgError(st, "ipmg_tables_1d")
     return np.array(buf[:n.value])
+
+
+def alu_peak(device=0, kind="ffma2", reps=5):
+    """Measured CUDA-core peak in TFLOP/s (ipmg_alu_peak): kind 'ffma2', 'ffma' or 'dfma'."""
+    lib = load()
+    out = ctypes.c_double()
+    st = lib.ipmg_alu_peak(device, {"ffma2": 0, "ffma": 1, "dfma": 2}[kind], reps, ctypes.byref(out))
+    if st != IPMG_OK:
+        raise IpmgError(st, "ipmg_alu_peak")
+    return out.value
 
 
 def partition(dim, coarse_cells, n_levels, nranks, rank, level, degree=1, min_local_dofs=0):
@@ -193,7 +204,8 @@ class Handle:
 
     def __init__(self, dim, degree, n_levels, coarse_cells=None, h0=0.5, smoother=MULTIPLICATIVE,
                  additive_omega=0.0, post_smooth_reverse=1, vcycle_precision=FP32, penalty_scale=1.0,
-                 device=0, stream=None, comm=None, kernel=KERNEL_FULL, basis=None, dist_min_dofs=0):
+                 device=0, stream=None, comm=None, kernel=KERNEL_FULL, basis=None, dist_min_dofs=0,
+                 boundary_penalty_scale=1.0):
         import torch
         self.lib = load()
         cfg = Config()
@@ -207,6 +219,7 @@ class Handle:
         cfg.penalty_scale, cfg.device = penalty_scale, device
         cfg.kernel = kernel
         cfg.dist_min_dofs = dist_min_dofs
+        cfg.boundary_penalty_scale = boundary_penalty_scale
         # the clamped kernel lives on the Hermite-type basis (the whole hierarchy)
         cfg.basis = (BASIS_HERMITE if kernel == KERNEL_CLAMPED else BASIS_LAGRANGE) if basis is None else basis
         if stream is None:
@@ -335,9 +348,10 @@ class Handle:
                     seconds=info.seconds, history=list(hist[:info.history_len]),
                     converged=(st == IPMG_OK))
 
-    def rhs(self, level, b):
+    def rhs(self, level, b, kind=0):
+        """b = int f phi_i: kind 0 f == 1, kind 1 the manufactured sin solution (ipmg_rhs)."""
         self._vec(b, level, FP64)
-        self._check(self.lib.ipmg_rhs(self.h, level, 0, _ptr(b)), "rhs")
+        self._check(self.lib.ipmg_rhs(self.h, level, kind, _ptr(b)), "rhs")
 
     def to_cellwise(self, level, x_lib, x_cw):
         p = self._prec(x_lib)
