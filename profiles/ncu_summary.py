@@ -61,6 +61,51 @@ def summarise(rep):
     return "\n".join(lines) + "\n"
 
 
+# flops per predicated-on thread instruction of the SASS opcodes that do floating-point work
+FLOPS = {"FFMA": 2, "FFMA2": 4, "FADD": 1, "FADD2": 2, "FMUL": 1, "FMUL2": 2, "DFMA": 2, "DADD": 1, "DMUL": 1,
+         "HFMA2": 0}
+
+
+def sass_mix(rep, launch=0):
+    """Per-opcode warp instructions and achieved flops of one launch, from the SASS source
+    page (ncu -i --page source --print-source sass): counters 'Instructions Executed' and
+    'Predicated-On Thread Instructions Executed' per SASS instruction."""
+    import re
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "--launch-skip", str(launch), "--launch-count", "1"], stdout=subprocess.PIPE,
+                         stderr=subprocess.DEVNULL, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hi = next(i for i, r in enumerate(rows) if "Address" in r)
+    hdr = rows[hi]
+    iS, iI = hdr.index("Source"), hdr.index("Instructions Executed")
+    iP = hdr.index("Predicated-On Thread Instructions Executed")
+    ops, flops, seen = defaultdict(int), defaultdict(float), set()
+    for r in rows[hi + 1:]:
+        if len(r) <= iP or not r[iI].strip().isdigit():
+            continue
+        if r[0] in seen:      # the page can list a function twice
+            continue
+        seen.add(r[0])
+        src = r[iS].strip()
+        op = re.sub(r"^@!?U?P\w+\s+", "", src).split()[0].split(".")[0] if src else "?"
+        ops[op] += int(r[iI])
+        flops[op] += FLOPS.get(op, 0) * int(r[iP] or 0)
+    return ops, flops
+
+
+def summarise_mix(rep, launch=0, top=16):
+    ops, flops = sass_mix(rep, launch)
+    tot = sum(ops.values())
+    fl = sum(flops.values())
+    lines = ["#### SASS mix of launch %d of %s (ncu source page)" % (launch, rep), "",
+             "warp instructions %d; floating-point work %.4g flop (FFMA/DFMA 2, FFMA2 4, FADD/FMUL 1, "
+             "packed x2 2 per thread instruction)" % (tot, fl), "",
+             "| opcode | warp inst | share | flop |", "|---|---|---|---|"]
+    for k, v in sorted(ops.items(), key=lambda kv: -kv[1])[:top]:
+        lines.append("| %s | %d | %.1f%% | %.4g |" % (k, v, 100.0 * v / tot, flops.get(k, 0)))
+    return "\n".join(lines) + "\n", tot, fl
+
+
 def launches(path):
     """Per-kernel share of the device time in an ncu --metrics gpu__time_duration.sum CSV."""
     text = open(path).read()
@@ -89,6 +134,9 @@ if __name__ == "__main__":
         for p in sys.argv[2:]:
             print("### %s\n" % p)
             print(launches(p))
+    elif sys.argv[1] == "--mix":
+        for p in sys.argv[2:]:
+            print(summarise_mix(p)[0])
     else:
         for p in sys.argv[1:]:
             print(summarise(p))

@@ -1,7 +1,10 @@
 """Profiling driver: one warm-up GMG-CG solve of the bench workload, then one
 solve inside an NVTX range "timed" (for ncu --nvtx --nvtx-include timed/).
 
-  python profiles/solve_once.py [--dim 2 --degree 7 --levels 10] [--fp64-vcycle]
+  python profiles/solve_once.py [--dim 3 --degree 4 --levels 8 --coarse 2,2,1] [--fp64-vcycle]
+
+Defaults: the bench headline workload C4 (BASELINE.json configs[3]); C2 is
+--dim 2 --degree 7 --levels 10 --coarse 2,2.
 """
 import argparse
 import os
@@ -17,12 +20,14 @@ from paper_2405_18982_b200 import ipmg  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--dim", type=int, default=2)
-    ap.add_argument("--degree", type=int, default=7)
-    ap.add_argument("--levels", type=int, default=10)
+    ap.add_argument("--dim", type=int, default=3)
+    ap.add_argument("--degree", type=int, default=4)
+    ap.add_argument("--levels", type=int, default=8)
+    ap.add_argument("--coarse", default="2,2,1")
     ap.add_argument("--fp64-vcycle", action="store_true")
     a = ap.parse_args()
-    h = ipmg.Handle(a.dim, a.degree, a.levels, vcycle_precision=ipmg.FP64 if a.fp64_vcycle else ipmg.FP32)
+    coarse = tuple(int(c) for c in a.coarse.split(","))[:a.dim]
+    h = ipmg.Handle(a.dim, a.degree, a.levels, coarse_cells=coarse, vcycle_precision=ipmg.FP64 if a.fp64_vcycle else ipmg.FP32)
     L = a.levels - 1
     n = h.ndofs(L)
     b = torch.empty(n, dtype=torch.float64, device="cuda")
