@@ -26,7 +26,7 @@ CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-I" + INCLUDE, "-I" + CSRC, "-I/usr/l
 SOURCES_CU = (["kernels_k%d.cu" % k for k in range(1, 8)] + ["kernels_dir_k%d.cu" % k for k in range(1, 8)] +
               ["blas.cu", "peak.cu"])
 SOURCES_CXX = ["fe1d.cpp", "comm.cpp", "ipmg.cpp"]
-HEADERS = ["common.cuh", "patch_kernels.cuh", "blas.cuh", "fe1d.hpp", "comm.hpp"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h")))   # every header is a dependency
 
 
 def _stale(obj, deps):

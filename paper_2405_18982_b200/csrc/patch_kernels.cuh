@@ -28,7 +28,10 @@
 #include "common.cuh"
 #include "fe1d.hpp"
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -2178,9 +2181,120 @@ cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void*
   return cudaGetLastError();
 }
 
+#if !IPMG_DIRICHLET
+#include "smooth_pair3.cuh"
+// 3D fp32 colour passes through the patch-pair kernel (smooth_pair3.cuh): bit k of
+// IPMG_PAIR3_DEGREES enables degree k (as measured); IPMG_PAIR3=0/1 in the
+// environment forces it off / on for every degree (A/B runs)
+#ifndef IPMG_PAIR3_DEGREES
+#define IPMG_PAIR3_DEGREES 0x10
+#endif
+#ifndef IPMG_PAIR3_NPAIR
+#define IPMG_PAIR3_NPAIR 1
+#endif
+inline bool pair3_enabled() {
+  static const int env = [] {
+    const char* e = std::getenv("IPMG_PAIR3");
+    return e ? std::atoi(e) : -1;
+  }();
+  return env >= 0 ? env != 0 : ((IPMG_PAIR3_DEGREES >> K) & 1) != 0;
+}
+// Thread -> line tables of the y and z passes: the lines of every pass, sorted by the
+// bank of their first element, are dealt round robin to the half warps, so a half
+// warp holds distinct banks whenever no bank class has more lines than there are
+// half warps (64-bit accesses are served per half warp).
+inline cudaError_t pair3_upload_tables() {
+  using namespace pair3;
+  static unsigned tab[3][2][NTMAX];
+  auto fill = [&](auto npc) {
+    constexpr int NPAIR = decltype(npc)::value;
+    constexpr int NT = PC<NPAIR>::NT, HW = NT / 16;
+    for (int d = 0; d < 2; ++d) {
+      std::vector<std::pair<int, int>> items;   // (bank, line id)
+      for (int q = 0; q < NPAIR; ++q)
+        for (int v = 0; v < NP; ++v)
+          for (int u = 0; u < NP; ++u) {
+            const int base = q * TSZ + u + (d == 0 ? S2 : S1) * v;
+            items.emplace_back(base % 16, q * NL + u + NP * v);
+          }
+      std::stable_sort(items.begin(), items.end(),
+                       [](const std::pair<int, int>& a, const std::pair<int, int>& b) { return a.first < b.first; });
+      for (int t = 0; t < NTMAX; ++t) tab[NPAIR - 1][d][t] = 0xffffffffu;
+      for (int k = 0; k < (int)items.size(); ++k) {
+        const int id = items[k].second, q = id / NL, l = id % NL, u = l % NP, v = l / NP;
+        const unsigned ofs = (unsigned)(q * TSZ + u + (d == 0 ? S2 : S1) * v);
+        tab[NPAIR - 1][d][16 * (k % HW) + k / HW] =
+            d == 0 ? ofs : (ofs | (unsigned)u << 16 | (unsigned)v << 20 | (unsigned)q << 24);
+      }
+    }
+  };
+  fill(std::integral_constant<int, 1>{});
+  fill(std::integral_constant<int, 2>{});
+  fill(std::integral_constant<int, 3>{});
+  return cudaMemcpyToSymbol(pair3::g_lines, tab, sizeof(tab));
+}
+// cell-index deltas of a launch in the parent-grouped layout: a cell (c0 + d) of a patch
+// whose lowest cell c0 has the colour's parities lies at cell(c0) + delta(d)
+inline pair3::Deltas pair3_deltas(const LevelGeom& g, int colour) {
+  pair3::Deltas d{};
+  const int PX = g.n[0] / 2, PY = g.n[1] / 2;
+  const int par[3] = {colour & 1, (colour >> 1) & 1, (colour >> 2) & 1};
+  auto delta = [&](int dx, int dy, int dz) {
+    const int dd[3] = {dx, dy, dz};
+    int f[3], r[3];
+    for (int a = 0; a < 3; ++a) {
+      const int v = par[a] + dd[a];
+      f[a] = v >= 0 ? v / 2 : -((1 - v) / 2);   // floor(v / 2)
+      r[a] = v - 2 * f[a];
+    }
+    return 8 * (f[0] + PX * (f[1] + PY * f[2])) + (r[0] - par[0]) + 2 * (r[1] - par[1]) + 4 * (r[2] - par[2]);
+  };
+  for (int q = 0; q < 8; ++q) d.pc[q] = delta(q & 1, (q >> 1) & 1, (q >> 2) & 1);
+  for (int k = 0; k < pair3::NNB; ++k) {
+    const int a = k >> 3, sd = (k >> 2) & 1, tc = k & 3;
+    const int sa = sd == 0 ? -1 : 2, t0 = tc & 1, t1 = (tc >> 1) & 1;
+    d.nb[k] = a == 0 ? delta(sa, t0, t1) : (a == 1 ? delta(t0, sa, t1) : delta(t0, t1, sa));
+  }
+  return d;
+}
+template <int NPAIR>
+cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
+  using C = pair3::PC<NPAIR>;
+  LevelGeom gg = g;
+  const int m0 = g.n[0] / 2 - (colour & 1);
+  const int m1 = g.n[1] / 2 - ((colour >> 1) & 1);
+  int m2 = slab_patches(g, 2, (colour >> 2) & 1);
+  m2 = m2 > 0 ? m2 : 0;
+  gg.znb = m2;
+  m2 = slab_sel_count(m2, g.zsel);
+  const dim3 grid((unsigned)((m0 + C::NPAT - 1) / C::NPAT), (unsigned)(m1 > 0 ? m1 : 0), (unsigned)m2);
+  if (grid.x * grid.y * grid.z == 0) return cudaErrorNotReady;   // empty patch lattice: the caller copies
+  cudaError_t e = set_smem(pair3::smooth_pair3_kernel<NPAIR>, C::SMEM);
+  if (e != cudaSuccess) return e;
+  const dim3 g2(grid.x + (colour != 0 && g.zsel != 2 ? 1 : 0), grid.y, grid.z);
+  pair3::smooth_pair3_kernel<NPAIR><<<g2, C::NT, C::SMEM, s>>>((const float*)xi, (const float*)b, (float*)xo, gg,
+                                                               colour, (int)grid.x, pair3_deltas(g, colour));
+  return cudaGetLastError();
+}
+#endif
+
 template <int D, typename T>
 cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
   using C = Cfg<D, T>;
+#if !IPMG_DIRICHLET
+  // the pair kernel's TMA copies need a 16-byte aligned x_in whose cell range ends on a
+  // 16-byte boundary (the copies are widened to 16-byte granularity)
+  // (zero-start passes, x_in == nullptr, stay on smooth_kernel: without face traces the
+  // pair kernel's fewer instructions do not make up for its lower occupancy, measured
+  // 3D k=4 colour 0 from zero 0.84 vs 0.94 ms)
+  if (D == 3 && sizeof(T) == 4 && xi != nullptr && pair3_enabled() && g.grouped && g.n[0] >= 2 && g.n[1] >= 2 &&
+      g.n[2] >= 2 &&
+      (reinterpret_cast<unsigned long long>(xi) & 15) == 0 && (g.ncells % 4) == 0 &&
+      (reinterpret_cast<unsigned long long>(xo) & 3) == 0) {
+    const cudaError_t e = launch_smooth_pair3<IPMG_PAIR3_NPAIR>(xi, b, xo, g, colour, s);
+    if (e != cudaErrorNotReady) return e;
+  }
+#endif
   LevelGeom gg = g;
   const dim3 grid = patch_grid<D, T>(gg, colour);
   // no neighbour staging (and less shared memory, more CTAs) when x_in == 0
@@ -2402,6 +2516,10 @@ inline cudaError_t upload(const FE1D& fe) {
   fill_tab(t32, fe);
   cudaError_t e = cudaMemcpyToSymbol(c_tab64, &t64, sizeof(t64));
   if (e != cudaSuccess) return e;
+#if !IPMG_DIRICHLET
+  e = pair3_upload_tables();
+  if (e != cudaSuccess) return e;
+#endif
   return cudaMemcpyToSymbol(c_tab32, &t32, sizeof(t32));
 }
 #if IPMG_DIRICHLET

@@ -106,6 +106,57 @@ def summarise_mix(rep, launch=0, top=16):
     return "\n".join(lines) + "\n", tot, fl
 
 
+def phases(rep, launch=0, units=1.0, top=8):
+    """Per-phase warp instructions of one launch: the SASS (ncu source page, in address
+    order) cut at every BAR.SYNC; counts are divided by `units` (e.g. the patches of the
+    launch).  Columns: executed warp instructions, stall samples, excess shared-memory
+    wavefronts (bank conflicts), L1 global tag requests, top opcodes."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "--launch-skip", str(launch), "--launch-count", "1"], stdout=subprocess.PIPE,
+                         stderr=subprocess.DEVNULL, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hi = next(i for i, r in enumerate(rows) if "Address" in r)
+    hdr = rows[hi]
+    iS, iI = hdr.index("Source"), hdr.index("Instructions Executed")
+    iW = hdr.index("Warp Stall Sampling (All Samples)")
+    iX = hdr.index("L1 Wavefronts Shared Excessive")
+    iL = hdr.index("L1 Tag Requests Global")
+    segs, cur, seen = [], None, set()
+    import re
+    for r in rows[hi + 1:]:
+        if len(r) <= iI or not r[iI].isdigit():
+            continue
+        if r[0] in seen:   # the page may list a launch twice
+            break
+        seen.add(r[0])
+        if cur is None:
+            cur = {"start": r[0][-5:], "inst": 0, "stall": 0, "exc": 0, "tag": 0, "ops": defaultdict(int)}
+        src = r[iS].strip()
+        op = re.sub(r"^@!?U?P\w+\s+", "", src).split()[0].split(".")[0] if src else "?"
+        n = int(r[iI])
+        cur["inst"] += n
+        cur["stall"] += int(r[iW] or 0)
+        cur["exc"] += int(r[iX] or 0)
+        cur["tag"] += int(r[iL] or 0)
+        cur["ops"][op] += n
+        if op == "BAR":
+            segs.append(cur)
+            cur = None
+    if cur:
+        segs.append(cur)
+    lines = ["#### Phases of launch %d of %s (per unit, unit = 1/%g of the launch)" % (launch, rep, units), "",
+             "| phase start | warp inst | stall samples | smem excess wavefronts | L1 global tags | top opcodes |",
+             "|---|---|---|---|---|---|"]
+    for g in segs:
+        if g["inst"] == 0:
+            continue
+        topo = ", ".join("%s %.0f" % (k, v / units) for k, v in sorted(g["ops"].items(), key=lambda kv: -kv[1])[:top])
+        lines.append("| %s | %.1f | %d | %.1f | %.1f | %s |" % (g["start"], g["inst"] / units, g["stall"],
+                                                             g["exc"] / units, g["tag"] / units, topo))
+    lines.append("| **total** | %.1f | | | | |" % (sum(g["inst"] for g in segs) / units))
+    return "\n".join(lines) + "\n"
+
+
 def launches(path):
     """Per-kernel share of the device time in an ncu --metrics gpu__time_duration.sum CSV."""
     text = open(path).read()
@@ -134,6 +185,8 @@ if __name__ == "__main__":
         for p in sys.argv[2:]:
             print("### %s\n" % p)
             print(launches(p))
+    elif sys.argv[1] == "--phases":   # --phases REP LAUNCH UNITS
+        print(phases(sys.argv[2], int(sys.argv[3]), float(sys.argv[4])))
     elif sys.argv[1] == "--mix":
         for p in sys.argv[2:]:
             print(summarise_mix(p)[0])

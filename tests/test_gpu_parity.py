@@ -64,7 +64,7 @@ def rel(a, b):
 CASES = [(2, 1, 4, None), (2, 2, 4, None), (2, 3, 4, None), (2, 4, 3, None), (2, 5, 3, None),
          (2, 6, 3, None), (2, 7, 3, None), (2, 3, 3, (2, 1)), (3, 1, 3, None), (3, 2, 3, None),
          (3, 3, 2, None), (3, 4, 2, None), (3, 5, 2, None), (3, 6, 2, None), (3, 7, 2, None),
-         (3, 2, 3, (2, 1, 2))]
+         (3, 2, 3, (2, 1, 2)), (3, 4, 3, None)]
 IDS = ["d%dk%dL%d%s" % (c[0], c[1], c[2], "" if c[3] is None else "c" + "".join(map(str, c[3]))) for c in CASES]
 
 

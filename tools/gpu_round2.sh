@@ -17,7 +17,7 @@ cat gpurun_out/bench_${TAG}.json; tail -3 gpurun_out/bench_${TAG}.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
   --csv --log-file gpurun_out/launches_${TAG}.csv python profiles/solve_once.py > gpurun_out/launches_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:smooth_kernel -s 1 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:smooth_pair3 -s 0 -c 2 \
   -o gpurun_out/prof_smooth_${TAG} -f python profiles/solve_once.py > gpurun_out/prof_smooth_${TAG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:vmult_kernel -s 0 -c 1 \
   -o gpurun_out/prof_vmult_${TAG} -f python profiles/solve_once.py > gpurun_out/prof_vmult_${TAG}.log 2>&1
