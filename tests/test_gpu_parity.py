@@ -57,7 +57,11 @@ def to_cw(h, level, t):
 
 
 def rel(a, b):
-    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+    """Relative error: the larger of the norm-wise ||a-b|| / ||b|| and the element-wise
+    max|a-b| / max|b| (a few wrong entries of a long vector fail the second)."""
+    nrm = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+    ele = np.abs(a - b).max() / max(np.abs(b).max(), 1e-300) if np.size(b) else 0.0
+    return max(nrm, ele)
 
 
 # (dim, k, n_levels, coarse) -- several CTAs, ragged last CTA, every boundary variant
@@ -182,8 +186,12 @@ def test_transfers_and_coarse(case):
         x0 = torch.empty(A0.shape[0], dtype=dtype, device="cuda")
         h.coarse_solve(to_lib(h, 0, b0, dtype), x0)
         ref = np.linalg.solve(A0, b0r)
-        # fp32: FD in single precision, conditioning of A_0 enters
-        assert rel(to_cw(h, 0, x0), ref) <= (tol if dtype == torch.float64 else 2e-5), dtype
+        # fp32: the solve is exact up to rounding, so its relative error is bounded by
+        # cond(A_0) times the unit roundoff (first-order perturbation bound); 1e-5 where
+        # that is smaller (cond(A_0): 12 for 2D k=1 ... 870 for 3D k=7)
+        if dtype == torch.float32:
+            tol = max(1e-5, np.linalg.cond(A0) * 2.0 ** -24)
+        assert rel(to_cw(h, 0, x0), ref) <= tol, dtype
 
 
 @pytest.mark.parametrize("case", [(2, 2, 4, None), (2, 7, 3, None), (3, 3, 3, None), (3, 2, 3, (2, 1, 2))],
