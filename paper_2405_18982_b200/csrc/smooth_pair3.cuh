@@ -196,7 +196,7 @@ __device__ __forceinline__ void load_b_rows(const float* __restrict__ b, const P
     }
   }
 #pragma unroll
-  for (int j = 0; j < NP; ++j) v[j] = mul2(make_float2(lo[0][j], lo[1][j]), f2(scale));
+  for (int j = 0; j < NP; ++j) v[j] = scale == 1.f ? make_float2(lo[0][j], lo[1][j]) : mul2(make_float2(lo[0][j], lo[1][j]), f2(scale));
 }
 
 template <int NPAT>
@@ -352,8 +352,9 @@ __device__ __forceinline__ void pair_body(const float* __restrict__ x_in, const 
     load_b_rows(b, P, dl, q0, i1, i2, (float)g.hinv, y);
     (void)brow;
 #else
+    const float hinv = (float)g.hinv;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) y[j] = brow[j];
+    for (int j = 0; j < NP; ++j) y[j] = mul2(brow[j], f2(hinv));
 #endif
     if (faces) {
       const float2* Fq = F + q0 * FPAIR;
@@ -506,7 +507,13 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
     }
     __syncthreads();
     const int lane = t & 31;
-    for (int e = t >> 5; e < NPAT * NNB; e += C::NT / 32) {
+    // unrolled: every copy gets its own address registers (a cp.async holds its source
+    // registers until it issues; a rolled loop serialised on them, ncu long_sb stalls)
+    constexpr int NW = C::NT / 32, PER = (NPAT * NNB + NW - 1) / NW;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = (t >> 5) + NW * i;
+      if (e >= NPAT * NNB) break;
       const unsigned long long ent = nba[e];
       if (ent == 0ull) continue;
       const unsigned long long src = ent & ~15ull;
@@ -523,7 +530,8 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
   float2 brow[NP];
   {
     const int q0 = t / NL, l0 = t % NL;
-    if (!IPMG_PAIR3_LATE_B && t < NPAIR * NL) load_b_rows(b, P, dl, q0, l0 % NP, l0 / NP, (float)g.hinv, brow);
+    // raw values: the h^{2-d} scaling waits for the loads, so it happens in the x pass
+    if (!IPMG_PAIR3_LATE_B && t < NPAIR * NL) load_b_rows(b, P, dl, q0, l0 % NP, l0 / NP, 1.f, brow);
   }
   bool allint = true;
 #pragma unroll
