@@ -323,7 +323,8 @@ def run_ours(args, rank, ws, local):
     prof_steps = max(1, min(args.steps, 3))
     h.profile(True)
     ms_prof, _ = time_solves(h, b, x, prof_steps, stream, dist, dev)
-    prof = {c: h.profile_read(c) for c in ("smooth", "vmult", "restrict", "prolong", "coarse", "blas")}
+    prof = {c: h.profile_read(c) for c in ("smooth", "vmult", "restrict", "prolong", "coarse", "blas",
+                                           "levels_below")}
     h.profile(False)
 
     # ---- components (separately timed, CUDA events): vmult fp64 and one smoother step fp32
@@ -473,7 +474,9 @@ def run_ours(args, rank, ws, local):
                                "%.1f ms/solve vs %.1f ms/solve unprofiled" % (prof_steps, ms_prof / prof_steps,
                                                                               ms_step),
                  "share_of_step": ms_s / ms_prof if ms_prof > 0 else None,
-                 "per_class_ms_share": {c: (v[1] / ms_prof if ms_prof > 0 else None) for c, v in prof.items()}})
+                 "per_class_ms_share": {c: (v[1] / ms_prof if ms_prof > 0 else None) for c, v in prof.items()},
+                 # the rest: host gaps of the solver loop (per-iteration scalar reads) and launch overheads
+                 "unattributed_share": (1.0 - sum(v[1] for v in prof.values()) / ms_prof) if ms_prof > 0 else None})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 CG / f32 V-cycle", "data": "synthetic (f=1 right-hand side)",

@@ -258,7 +258,8 @@ ipmg_status ipmg_synchronize(ipmg_handle *h);
  * handle's stream around each launch); 0 disables.  ipmg_profile_read
  * synchronises and returns, for kernel_class (0 smoother colour pass,
  * 1 operator apply / residual, 2 residual+restrict, 3 prolongate+add,
- * 4 coarse solve, 5 vector kernels, 6 additive colour pass), the number of
+ * 4 coarse solve, 5 vector kernels, 6 additive colour pass, 7 the levels below the
+ * finest in a V-cycle, timed as one block: the CUDA-graph replay of levels L-1..0), the number of
  * recorded launches, their summed device time in ms, and their summed
  * ALGORITHMIC HBM bytes.  ipmg_launch_count: total
  * kernels this handle has launched. */

@@ -82,7 +82,7 @@ ipmg::KernelSet kernel_set_dir(int k) {
 }  // namespace
 
 enum KClass { KC_SMOOTH = 0, KC_VMULT = 1, KC_RESTRICT = 2, KC_PROLONG = 3, KC_COARSE = 4, KC_BLAS = 5,
-              KC_ADDITIVE = 6, KC_N = 7 };
+              KC_ADDITIVE = 6, KC_BELOW = 7, KC_N = 8 };
 
 struct ipmg_handle {
   ipmg_config cfg{};
@@ -395,7 +395,16 @@ struct ipmg_handle {
   // ~100 small kernels) replayed from a CUDA graph captured on first use; the
   // finest level's kernels are launched directly (so ipmg_profile still times
   // them).  Not with a communicator that cannot be captured (in-process team).
+  // timed as one record of class KC_BELOW (the levels below the finest, ipmg_profile)
   ipmg_status run_coarse_vcycle(int prec) {
+    ipmg_status inner = IPMG_OK;
+    const ipmg_status st = run(KC_BELOW, nlev - 1, 0.0, 0, [&] {
+      inner = run_coarse_vcycle_impl(prec);
+      return cudaSuccess;
+    }, "levels below the finest");
+    return inner != IPMG_OK ? inner : st;
+  }
+  ipmg_status run_coarse_vcycle_impl(int prec) {
     const int L = nlev - 2;
     if (!use_graphs || (comm && !comm->capturable())) return vcycle_level(L, prec);
     if (!vgraph[prec]) {

@@ -135,7 +135,15 @@ struct Cfg {
 #ifndef IPMG_PPC3_NC
 #define IPMG_PPC3_NC 0   // restrict IPMG_PPC3 to this NC (0: all)
 #endif
-  static constexpr int PPC = (D == 3 && IPMG_PPC3 > 0 && (IPMG_PPC3_NC == 0 || IPMG_PPC3_NC == NC))
+#ifndef IPMG_PPC3_64
+#define IPMG_PPC3_64 0   // > 0: patches per CTA of every 3D fp64 kernel (experiments); 0: as measured
+#endif
+  // 3D fp64 kernels (the CG operator): 2 patches per CTA for k = 4 and 7 (measured,
+  // tools/gpu_ab_vmult.sh: 3D k=4 fp64 operator 3.20 -> 3.03 ms, k=7 2.19 -> 1.96 ms;
+  // neutral or slower for k = 2, 3, 5, 6; 3 patches slower everywhere)
+  static constexpr int PPC = (D == 3 && sizeof(T) == 8 && IPMG_PPC3_64 > 0) ? IPMG_PPC3_64
+                           : (D == 3 && sizeof(T) == 8 && IPMG_PPC3_64 == 0 && (NC == 5 || NC == 8)) ? 2
+                           : (D == 3 && IPMG_PPC3 > 0 && (IPMG_PPC3_NC == 0 || IPMG_PPC3_NC == NC))
                                  ? IPMG_PPC3
                                  : ((GT / G) > 1 ? (GT / G) : 1);   // patches per CTA
   static constexpr int GROUPS = PPC * G;

@@ -30,7 +30,8 @@ EXPORTS = ["ipmg_config_default", "ipmg_create", "ipmg_destroy", "ipmg_level_inf
            "ipmg_profile", "ipmg_profile_read", "ipmg_launch_count", "ipmg_level_partition", "ipmg_partition",
            "ipmg_nccl_unique_id", "ipmg_comm_create_nccl", "ipmg_comm_create_local", "ipmg_comm_destroy", "ipmg_alu_peak"]
 
-KERNEL_CLASSES = {"smooth": 0, "vmult": 1, "restrict": 2, "prolong": 3, "coarse": 4, "blas": 5, "additive": 6}
+KERNEL_CLASSES = {"smooth": 0, "vmult": 1, "restrict": 2, "prolong": 3, "coarse": 4, "blas": 5, "additive": 6,
+                  "levels_below": 7}
 
 
 class Config(ctypes.Structure):
