@@ -450,15 +450,33 @@ __device__ __forceinline__ void pair_body(const float* __restrict__ x_in, const 
 template <int NPAIR>
 __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
     smooth_pair3_kernel(const float* __restrict__ x_in, const float* __restrict__ b, float* __restrict__ x_out,
-                        LevelGeom g, int colour, int nbx, const __grid_constant__ Deltas dl) {
+                        LevelGeom g, int colour, int gx, int gy, int gz, int ty, int ncopy,
+                        const __grid_constant__ Deltas dl) {
   using C = PC<NPAIR>;
   constexpr int NPAT = C::NPAT;
-  if ((int)blockIdx.x >= nbx) {   // the extra column of CTAs copies the cells the colour does not cover
-    const long long qq = blockIdx.y + (long long)gridDim.y * blockIdx.z;
-    copy_uncovered_part<3, float>(x_in, x_out, g, colour, qq * blockDim.x + threadIdx.x,
-                                  (long long)gridDim.y * gridDim.z * blockDim.x);
+  // 1D grid over the colour's pair lattice (gx pairs per row, gy rows, gz planes) in tiles
+  // of ty rows: x fastest, then the tile's rows, then the planes -- a patch's z-neighbours
+  // are gx*ty CTAs away instead of a whole plane (gx*gy), so the neighbour cells of its
+  // z-faces are still in L2 (ncu: 12.7 GB DRAM reads per C4 pass, 8.4 GB algorithmic);
+  // then ncopy CTAs copy the cells the colour does not cover
+  const long long item = blockIdx.x, nitems = (long long)gx * gy * gz;
+  if (item >= nitems) {
+    copy_uncovered_part<3, float>(x_in, x_out, g, colour, (item - nitems) * blockDim.x + threadIdx.x,
+                                  (long long)ncopy * blockDim.x);
     return;
   }
+  int bxi, byi, jz;
+  {
+    const long long per_tile = (long long)gx * ty * gz, full = gy / ty;
+    const long long tile = item / per_tile;
+    const int rows = tile < full ? ty : gy - (int)full * ty;
+    const long long r = item - tile * per_tile;
+    bxi = (int)(r % gx);
+    const long long r2 = r / gx;
+    byi = (int)tile * ty + (int)(r2 % rows);
+    jz = (int)(r2 / rows);
+  }
+  const int bzi = g.zsel == 0 ? jz : (g.zsel == 1 ? jz + 1 : (jz == 0 ? 0 : g.znb - 1));
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* X = reinterpret_cast<float2*>(smem_raw);
   float* NBs = reinterpret_cast<float*>(smem_raw);                       // aliased with X
@@ -476,11 +494,10 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
   // patches of the CTA (x-blocks of NPAT patches, row by, plane bz)
   if (t < NPAT) {
     const int p = t;
-    const int by = blockIdx.y, bz = slab_block<3>(g);
     const int m0 = g.n[0] / 2 - (colour & 1);
-    const int c0y = ((colour >> 1) & 1) + 2 * by;
-    const int c0z = slab_first(g, (colour >> 2) & 1) + 2 * bz;
-    const int j0 = blockIdx.x * NPAT + p;
+    const int c0y = ((colour >> 1) & 1) + 2 * byi;
+    const int c0z = slab_first(g, (colour >> 2) & 1) + 2 * bzi;
+    const int j0 = bxi * NPAT + p;
     const bool valid = j0 < m0;
     const int c0x = (colour & 1) + 2 * (valid ? j0 : 0);
     P.base[p] = (int)cell_offset_cells(g, c0x, c0y, c0z);

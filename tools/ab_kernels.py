@@ -30,7 +30,8 @@ def timeit(fn, reps=20, warm=3):
 
 def main():
     dim, k, nl = (int(a) for a in sys.argv[1:4]) if len(sys.argv) >= 4 else (2, 7, 10)
-    h = ipmg.Handle(dim, k, nl, vcycle_precision=ipmg.FP32)
+    coarse = tuple(int(c) for c in os.environ["AB_COARSE"].split(",")) if os.environ.get("AB_COARSE") else None
+    h = ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=ipmg.FP32)
     L = nl - 1
     n = h.ndofs(L)
     nc = h.ndofs(L - 1)
@@ -46,7 +47,7 @@ def main():
     res["vmult32_ms"] = timeit(lambda: h.vmult(L, x32, o32))
     res["restrict32_ms"] = timeit(lambda: h.residual_restrict(L, x32, b32, rc))
     res["prolong32_ms"] = timeit(lambda: h.prolongate_add(L, rc, o32))
-    hd = ipmg.Handle(dim, k, nl, vcycle_precision=ipmg.FP32, kernel=ipmg.KERNEL_DIRICHLET)
+    hd = ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=ipmg.FP32, kernel=ipmg.KERNEL_DIRICHLET)
     res["smooth_dir_c1_ms"] = timeit(lambda: hd.smooth_colour(L, x32, b32, o32, 1))
     xs = x32.clone()
     res["smooth_step_ms"] = timeit(lambda: h.smooth(L, xs, b32))

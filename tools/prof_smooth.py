@@ -11,7 +11,8 @@ import torch  # noqa: E402
 from paper_2405_18982_b200 import ipmg  # noqa: E402
 
 dim, k, nl = (int(a) for a in sys.argv[1:4]) if len(sys.argv) >= 4 else (2, 7, 10)
-h = ipmg.Handle(dim, k, nl, vcycle_precision=ipmg.FP32)
+coarse = tuple(int(c) for c in os.environ["AB_COARSE"].split(",")) if os.environ.get("AB_COARSE") else None
+h = ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=ipmg.FP32)
 L = nl - 1
 n = h.ndofs(L)
 x = torch.empty(n, device="cuda").uniform_(-1, 1)
