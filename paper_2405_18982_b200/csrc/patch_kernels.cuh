@@ -2200,10 +2200,6 @@ cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void*
 #ifndef IPMG_PAIR3_NPAIR
 #define IPMG_PAIR3_NPAIR 1
 #endif
-#ifndef IPMG_PAIR3_TY
-#define IPMG_PAIR3_TY 8   // rows per traversal tile (0: whole planes, the plain x-y-z order); 8 measured at C4:
-                          // DRAM reads per pass 12.74 -> 8.96 GB (8.4 algorithmic), time unchanged
-#endif
 inline bool pair3_enabled() {
   static const int env = [] {
     const char* e = std::getenv("IPMG_PAIR3");
@@ -2280,21 +2276,13 @@ cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const L
   gg.znb = m2;
   m2 = slab_sel_count(m2, g.zsel);
   const int gx = (m0 + C::NPAT - 1) / C::NPAT, gy = m1 > 0 ? m1 : 0, gz = m2;
-  const long long nitems = (long long)gx * gy * gz;
-  if (nitems == 0) return cudaErrorNotReady;   // empty patch lattice: the caller copies
+  if ((long long)gx * gy * gz == 0) return cudaErrorNotReady;   // empty patch lattice: the caller copies
   cudaError_t e = set_smem(pair3::smooth_pair3_kernel<NPAIR>, C::SMEM);
   if (e != cudaSuccess) return e;
-  // rows per traversal tile (L2 locality of the z-face neighbours; IPMG_PAIR3_TY overrides)
-  static const int ty_env = [] {
-    const char* v = std::getenv("IPMG_PAIR3_TY");
-    return v ? std::atoi(v) : -1;
-  }();
-  int ty = ty_env > 0 ? ty_env : IPMG_PAIR3_TY;
-  if (ty <= 0 || ty > gy) ty = gy;
-  const int ncopy = (colour != 0 && g.zsel != 2) ? gy * gz : 0;   // CTAs copying the uncovered cells
-  pair3::smooth_pair3_kernel<NPAIR><<<(unsigned)(nitems + ncopy), C::NT, C::SMEM, s>>>(
-      (const float*)xi, (const float*)b, (float*)xo, gg, colour, gx, gy, gz, ty, ncopy > 0 ? ncopy : 1,
-      pair3_deltas(g, colour));
+  constexpr int TY = pair3::TY;
+  const dim3 grid((unsigned)(gx + (colour != 0 && g.zsel != 2 ? 1 : 0)), (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
+  pair3::smooth_pair3_kernel<NPAIR><<<grid, C::NT, C::SMEM, s>>>((const float*)xi, (const float*)b, (float*)xo, gg,
+                                                               colour, gx, gy, pair3_deltas(g, colour));
   return cudaGetLastError();
 }
 #endif

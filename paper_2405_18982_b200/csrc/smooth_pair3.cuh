@@ -39,7 +39,10 @@ constexpr int H = NP / 2;
 constexpr int S1 = NP + 1;                // float2 strides of the pair tensor: x 1, y S1, z S2
 constexpr int S2 = NP * S1;               // S2 = NP S1 and S1 odd: x-line t has base S1 t (mod 16)
 constexpr int TSZ = NP * S2;              // pair pitch = S1 NL: the sequence continues across pairs
-constexpr int FROW = NP + 1;              // face array: t1 fastest, t2 rows of FROW float2
+#ifndef IPMG_PAIR3_FROW_PAD
+#define IPMG_PAIR3_FROW_PAD 0   // face-array row padding (0: rows of NP; keeps 6 CTAs/SM at k = 4)
+#endif
+constexpr int FROW = NP + IPMG_PAIR3_FROW_PAD;   // face array: t1 fastest, t2 rows of FROW float2
 constexpr int FARR = NP * FROW + ((10 - (NP * FROW) % 16) + 16) % 16;   // array pitch = 10 (mod 16)
 constexpr int FPAIR = 12 * FARR;          // (a, side, kind) arrays per pair
 constexpr int NNB = 24;                   // face-neighbour cells per patch
@@ -447,35 +450,31 @@ __device__ __forceinline__ void pair_body(const float* __restrict__ x_in, const 
 #ifndef IPMG_PAIR3_MINB
 #define IPMG_PAIR3_MINB 0   // minimum resident CTAs per SM requested from ptxas (0: none)
 #endif
+#ifndef IPMG_PAIR3_TY
+#define IPMG_PAIR3_TY 8   // rows per traversal tile (see the kernel); C4 DRAM reads 12.74 -> 8.96 GB
+#endif
+constexpr int TY = IPMG_PAIR3_TY;
 template <int NPAIR>
 __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
     smooth_pair3_kernel(const float* __restrict__ x_in, const float* __restrict__ b, float* __restrict__ x_out,
-                        LevelGeom g, int colour, int gx, int gy, int gz, int ty, int ncopy,
+                        LevelGeom g, int colour, int gx, int gy,
                         const __grid_constant__ Deltas dl) {
   using C = PC<NPAIR>;
   constexpr int NPAT = C::NPAT;
-  // 1D grid over the colour's pair lattice (gx pairs per row, gy rows, gz planes) in tiles
-  // of ty rows: x fastest, then the tile's rows, then the planes -- a patch's z-neighbours
-  // are gx*ty CTAs away instead of a whole plane (gx*gy), so the neighbour cells of its
-  // z-faces are still in L2 (ncu: 12.7 GB DRAM reads per C4 pass, 8.4 GB algorithmic);
-  // then ncopy CTAs copy the cells the colour does not cover
-  const long long item = blockIdx.x, nitems = (long long)gx * gy * gz;
-  if (item >= nitems) {
-    copy_uncovered_part<3, float>(x_in, x_out, g, colour, (item - nitems) * blockDim.x + threadIdx.x,
-                                  (long long)ncopy * blockDim.x);
+  // Grid (gx + 1, TY * gz, ceil(gy / TY)) over the colour's pair lattice (gx pairs per
+  // row, gy rows, gz planes): the hardware order (x fastest, then y, then z) walks tiles of
+  // TY rows -- x, then the tile's rows, then the planes -- so a patch's z-neighbours are
+  // gx*TY CTAs away instead of a whole plane (gx*gy) and the neighbour cells of its z-faces
+  // are still in L2 (ncu: C4 pass DRAM reads 12.74 -> 8.96 GB, 8.4 GB algorithmic).  The
+  // extra x column copies the cells the colour does not cover.
+  if ((int)blockIdx.x >= gx) {
+    const long long qq = blockIdx.y + (long long)gridDim.y * blockIdx.z;
+    copy_uncovered_part<3, float>(x_in, x_out, g, colour, qq * blockDim.x + threadIdx.x,
+                                  (long long)gridDim.y * gridDim.z * blockDim.x);
     return;
   }
-  int bxi, byi, jz;
-  {
-    const long long per_tile = (long long)gx * ty * gz, full = gy / ty;
-    const long long tile = item / per_tile;
-    const int rows = tile < full ? ty : gy - (int)full * ty;
-    const long long r = item - tile * per_tile;
-    bxi = (int)(r % gx);
-    const long long r2 = r / gx;
-    byi = (int)tile * ty + (int)(r2 % rows);
-    jz = (int)(r2 / rows);
-  }
+  const int bxi = blockIdx.x, byi = (int)blockIdx.z * TY + (int)(blockIdx.y % TY), jz = (int)(blockIdx.y / TY);
+  if (byi >= gy) return;   // the last tile's missing rows
   const int bzi = g.zsel == 0 ? jz : (g.zsel == 1 ? jz + 1 : (jz == 0 ? 0 : g.znb - 1));
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* X = reinterpret_cast<float2*>(smem_raw);
