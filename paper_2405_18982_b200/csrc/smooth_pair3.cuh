@@ -43,7 +43,10 @@ constexpr int TSZ = NP * S2;              // pair pitch = S1 NL: the sequence co
 #define IPMG_PAIR3_FROW_PAD 0   // face-array row padding (0: rows of NP; keeps 6 CTAs/SM at k = 4)
 #endif
 constexpr int FROW = NP + IPMG_PAIR3_FROW_PAD;   // face array: t1 fastest, t2 rows of FROW float2
-constexpr int FARR = NP * FROW + ((10 - (NP * FROW) % 16) + 16) % 16;   // array pitch = 10 (mod 16)
+// array pitch: searched over the face-array accesses (trace-unit writes, the t2 pass, the
+// x-pass reads) for the fewest excess 64-bit shared wavefronts: +1 for NP = 10 (FARR 101:
+// 190 excess per pair-pass against 420 at 106), otherwise 10 (mod 16)
+constexpr int FARR = (NP == 10 && FROW == 10) ? 101 : NP * FROW + ((10 - (NP * FROW) % 16) + 16) % 16;
 constexpr int FPAIR = 12 * FARR;          // (a, side, kind) arrays per pair
 constexpr int NNB = 24;                   // face-neighbour cells per patch
 // neighbour slot: the TMA copy covers the cell from the 16-byte boundary below it,
