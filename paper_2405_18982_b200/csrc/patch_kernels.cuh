@@ -103,10 +103,16 @@ template <int D, typename T>
 struct Cfg {
   // lines per thread: fp32 2 for k <= 3, 1 for k >= 4 (C3 sweep: 3D k=4/5 smoother
   // +10 %, 2D k=7 solve 30.4 -> 29.2 ms); fp64 1
+#ifndef IPMG_R64
+#define IPMG_R64 0   // lines per thread of the fp64 kernels (0: as measured -- 2 for 3D k=7, else 1)
+#endif
+  // fp64: 3D k=7 operator 1.96 -> 1.68 ms with 2 lines per thread (and 1 patch per CTA);
+  // slower for k = 2, 4, 5, 6, equal for k = 3 (tools/gpu_ab_vmult.sh)
+  static constexpr int R64 = IPMG_R64 > 0 ? IPMG_R64 : ((D == 3 && NC == 8) ? 2 : 1);
 #ifdef IPMG_R32
-  static constexpr int R = sizeof(T) == 4 ? IPMG_R32 : 1;
+  static constexpr int R = sizeof(T) == 4 ? IPMG_R32 : R64;
 #else
-  static constexpr int R = (sizeof(T) == 4 && NC <= 4) ? 2 : 1;
+  static constexpr int R = (sizeof(T) == 4 && NC <= 4) ? 2 : (sizeof(T) == 8 ? R64 : 1);
 #endif
   static constexpr int RP = NP + 1;                           // row pitch (odd)
   static constexpr int NL = (D == 2) ? NP : NP * NP;          // lines per direction per patch
@@ -138,11 +144,11 @@ struct Cfg {
 #ifndef IPMG_PPC3_64
 #define IPMG_PPC3_64 0   // > 0: patches per CTA of every 3D fp64 kernel (experiments); 0: as measured
 #endif
-  // 3D fp64 kernels (the CG operator): 2 patches per CTA for k = 4 and 7 (measured,
-  // tools/gpu_ab_vmult.sh: 3D k=4 fp64 operator 3.20 -> 3.03 ms, k=7 2.19 -> 1.96 ms;
-  // neutral or slower for k = 2, 3, 5, 6; 3 patches slower everywhere)
+  // 3D fp64 kernels (the CG operator): 2 patches per CTA for k = 4 (measured,
+  // tools/gpu_ab_vmult.sh: 3D k=4 fp64 operator 3.20 -> 3.03 ms; neutral or slower for
+  // k = 2, 3, 5, 6; 3 patches slower everywhere; k = 7 takes 2 lines per thread instead)
   static constexpr int PPC = (D == 3 && sizeof(T) == 8 && IPMG_PPC3_64 > 0) ? IPMG_PPC3_64
-                           : (D == 3 && sizeof(T) == 8 && IPMG_PPC3_64 == 0 && (NC == 5 || NC == 8)) ? 2
+                           : (D == 3 && sizeof(T) == 8 && IPMG_PPC3_64 == 0 && NC == 5) ? 2
                            : (D == 3 && IPMG_PPC3 > 0 && (IPMG_PPC3_NC == 0 || IPMG_PPC3_NC == NC))
                                  ? IPMG_PPC3
                                  : ((GT / G) > 1 ? (GT / G) : 1);   // patches per CTA
