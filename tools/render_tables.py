@@ -12,7 +12,7 @@ def c3(path):
     out = ["### C3 sweep (BASELINE.json configs[2]): 3D SIPG k=1..7, ~130M dofs, one B200", "",
            "`python tools/sweep_c3.py` (CUDA events, 3 warm-up + 10 timed calls, vectors > L2). Roofline: algorithmic "
            "bytes (vmult 2s, smoother step 2^d*3s per dof) vs MEASURED_PEAKS hbm_gbs; flops (vmult 14(k+1)+48, "
-           "smoother `bench.smoother_flops_per_dof`) vs the CUDA-core peak from unit counts.", "",
+           "smoother `bench.smoother_flops_per_dof`) vs the CUDA-core peaks measured live (ipmg_alu_peak: FFMA2 for fp32, DFMA for fp64).", "",
            "| k | cells | dofs | vmult fp64 GDoF/s (bound, frac) | vmult fp32 | smoother step fp64 | smoother step fp32 "
            "| mixed GMG-CG solve ms (its) |", "|---|---|---|---|---|---|---|---|"]
     for r in rows:

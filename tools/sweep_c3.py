@@ -8,8 +8,7 @@ plus one mixed-precision GMG-CG solve per degree.
 Sizes: power-of-two boxes closest to 2^27 dofs.
 Timing: CUDA events on the handle's stream, 3 warm-up + 10 timed calls; all
 vectors are larger than L2.  Peaks: HBM from MEASURED_PEAKS.json; FP32/FP64
-CUDA-core peaks from the unit counts (148 SMs x 128 / 64 lanes x 2 flops x
-max SM clock), as in bench.py.
+CUDA-core peaks measured live (ipmg_alu_peak: FFMA2 / DFMA), as in bench.py.
 """
 import argparse
 import json
@@ -47,9 +46,12 @@ def timeit(stream, fn, reps=10, warm=3):
     return e0.elapsed_time(e1) / reps
 
 
+ALU = {}   # measured CUDA-core peaks (TF/s) per precision, filled in main()
+
+
 def roof(bytes_, flops, ms, prec, peaks):
     hbm = peaks["hbm_gbs"]
-    alu = bench.alu_peak_tflops(prec, peaks)
+    alu = ALU[prec]
     t_b, t_f = bytes_ / (hbm * 1e9), flops / (alu * 1e12)
     if t_b >= t_f:
         return {"bound": "hbm", "achieved": bytes_ / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
@@ -64,6 +66,8 @@ def main():
     ap.add_argument("--degrees", default="1,2,3,4,5,6,7")
     a = ap.parse_args()
     peaks, src = bench.measured_peaks()
+    ALU["fp32"] = ipmg.alu_peak(0, "ffma2")
+    ALU["fp64"] = ipmg.alu_peak(0, "dfma")
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     out = open(a.out, "w")
     for k in [int(v) for v in a.degrees.split(",")]:
