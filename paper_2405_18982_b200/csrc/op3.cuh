@@ -1,0 +1,349 @@
+// 3D fp64 operator apply, one colour-0 vertex patch per CTA, staged (included by
+// patch_kernels.cuh inside namespace ipmg::kdeg<K> after smooth_pair3.cuh; full kernel only).
+//
+// Same operator as vmult_kernel<3, double> (Fig. 1 patch-wise
+// integration; Kronecker sum of the patch matrices PAPER.md:118-126; face terms of the
+// SIPG bilinear form PAPER.md:90-95): for every colour-0 patch j (the colour-0 patches
+// tile the mesh, so each writes only its own cells -- no atomics)
+//     y_j = h^{d-2} (A_jj x_j + C_j x_ext)      (or b_j - that, for a residual),
+//   A_jj x = M2 (L1 M0 x + M1 L0 x) + L2 (M1 M0 x)   (patch-local 1D mass M, stiffness +
+//   face terms L, boundary variants per direction), C_j x_ext from the traces of the 24
+//   face-neighbour cells.  What differs from vmult_kernel is how it reaches the data
+//   (ncu of vmult_kernel<3,double> at k = 4: 27 % of the stall samples long_sb -- the
+//   neighbour traces and the x rows were read straight from global memory by dependent
+//   loads, 5.8 k warp instructions per patch):
+//
+//  * the patch's own 8 cells and its 24 face-neighbour cells are copied into shared
+//    memory with 16-byte cp.async at the start (one warp per cell, lanes on consecutive
+//    chunks, the copy widened to the 16-byte boundaries around the cell: 63 chunks per
+//    1000-byte cell); the line tensors X, T1 alias the neighbour copies once the traces
+//    are formed;
+//  * trace units (family a, side s, tangential cell h, second tangential index ic) read a
+//    5x5 block of a staged neighbour cell and form u (face value) and u' (normal
+//    derivative) at NC face points; the tangential masses the operator needs are applied
+//    where the sum factorisation does not apply them anyway: the x-normal family is
+//    injected into L0 x in the x pass (M1, M2 follow), the y-normal family into the y
+//    pass (needs M along x), the z-normal family into the z pass (needs M along x and y);
+//  * y- and z-lines are dealt to threads by the bank-sorted tables of the pair smoother
+//    (same strides, same 8-byte elements);
+//  * the z pass writes the result straight to global memory and forms the fused x.y of
+//    CG from the staged x.
+#if !IPMG_DIRICHLET
+namespace op3 {
+#ifndef IPMG_OP3_STAGE_OWN
+#define IPMG_OP3_STAGE_OWN 0   // 1: the own cells are staged with the neighbours (x pass reads shared memory):
+                               // 42 KB, 5 CTAs/SM, 3D k=4 128^3 operator 2.50 ms; 0: x rows from global, 6 CTAs/SM, 2.41 ms
+#endif
+constexpr int NL = NP * NP;
+constexpr int CELL = NC * NC * NC;
+constexpr int S1 = NP + 1, S2 = NP * S1, TSZ = NP * S2;   // line tensor strides (as pair3)
+constexpr int FROW = NP;                                    // face array: t1 fastest, t2 rows
+constexpr int FARR = NP * FROW + 1;                         // array pitch (odd)
+constexpr int NNB = 24;
+// a staged cell: the copy covers the cell from the 16-byte boundary at or below its start
+// to the one at or above its end; 8-byte cell starts make that ceil((8 CELL + 8) / 16)
+// chunks at most
+constexpr int CHUNKS = (8 * CELL + 8 + 15) / 16;
+constexpr int SLOT = 2 * CHUNKS;                            // doubles per slot
+constexpr int NT = (((NL > 12 * NP ? NL : 12 * NP) + 31) / 32) * 32;   // a line / trace unit per thread
+static_assert(NT <= pair3::NTMAX, "line tables");
+constexpr int NSTAGE = NNB + (IPMG_OP3_STAGE_OWN ? 8 : 0);  // staged cells
+constexpr size_t NBB = sizeof(double) * (size_t)NNB * SLOT;
+constexpr size_t XB = sizeof(double) * 2 * (size_t)TSZ;     // X and T1 (alias the neighbour slots)
+constexpr size_t OWNB = IPMG_OP3_STAGE_OWN ? sizeof(double) * 8 * (size_t)SLOT : 0;
+constexpr size_t FB = sizeof(double) * 12 * (size_t)FARR;
+constexpr size_t SMEM = NBB + OWNB + FB;
+static_assert(XB <= NBB, "op3: X, T1 alias the neighbour slots");
+
+__device__ __forceinline__ int farr(int a, int s, int kind) { return ((a * 2 + s) * 2 + kind) * FARR; }
+
+// Trace unit of family A (compile-time: one code path per family, no selects):
+// u[lb] = x(face node), du[lb] = sum_j phi_j'(face) x_j of the neighbour across face
+// (A, s) at the NC face points lb along t1 in t1-cell h, second tangential index ic;
+// families 1 and 2 get the cell mass along t1 (= x) applied.
+template <int A>
+__device__ __forceinline__ void trace_unit(double* F, const double* c, bool exists, int s, int h, int ic) {
+  const TabData<K, double>& tb = tab<double>();
+  const int lc = ic % NC;
+  double u[NC], du[NC];
+  if (exists) {
+    const int jf = s == 0 ? NC - 1 : 0;   // face node: the neighbour's last node (low side), first (high)
+    // element (normal j, point lb) of the 5x5 block at c + PS * lb + NS * j + TS * lc
+    constexpr int PS = A == 0 ? NC : 1;            // point stride (t1 = y for A = 0, x otherwise)
+    constexpr int NS = A == 0 ? 1 : (A == 1 ? NC : NC * NC);
+    constexpr int TS = A == 2 ? NC : NC * NC;      // second tangential (t2 = z, z, y)
+    const double* b0 = c + TS * lc;
+    double v[NC][NC];   // [point][normal]
+#pragma unroll
+    for (int lb = 0; lb < NC; ++lb)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) v[lb][j] = b0[PS * lb + NS * j];
+#pragma unroll
+    for (int lb = 0; lb < NC; ++lb) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) acc = fma(s == 0 ? tb.d1[j] : tb.d0[j], v[lb][j], acc);
+      du[lb] = acc;
+      u[lb] = s == 0 ? v[lb][NC - 1] : v[lb][0];
+    }
+    (void)jf;
+  } else {
+#pragma unroll
+    for (int lb = 0; lb < NC; ++lb) u[lb] = du[lb] = 0.0;
+  }
+  double* fu = F + farr(A, s, 0) + h * NC + FROW * ic;
+  double* fd = F + farr(A, s, 1) + h * NC + FROW * ic;
+  if (A == 0) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      fu[i] = u[i];
+      fd[i] = du[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      double mu = 0.0, md = 0.0;
+#pragma unroll
+      for (int lb = 0; lb < NC; ++lb) {
+        mu = fma(tb.M[lb][i], u[lb], mu);
+        md = fma(tb.M[lb][i], du[lb], md);
+      }
+      fu[i] = mu;
+      fd[i] = md;
+    }
+  }
+}
+
+// second tangential mass (along y) of the z-normal family: line e of 40 = (side, kind, x index o)
+__device__ __forceinline__ void t2_mass(double* F, int e) {
+  const int o = e % NP, sk = e / NP;   // sk = side * 2 + kind
+  double* base = F + farr(2, sk >> 1, sk & 1) + o;
+  double v[1][NP], w[1][NP];
+  load_lines<NP, 1>(base, 0, FROW, v);
+  mv<NP, NP, MassP<double>, 1>(v, w);
+  store_lines<NP, 1>(base, 0, FROW, w);
+}
+
+// injection of face family a at tangential position pos into a line along a (operator sign +)
+__device__ __forceinline__ void inject(double (&y)[1][NP], const double* F, int a, int pos) {
+  const TabData<K, double>& tb = tab<double>();
+  const double ul = F[farr(a, 0, 0) + pos], dl = F[farr(a, 0, 1) + pos];
+  const double uh = F[farr(a, 1, 0) + pos], dh = F[farr(a, 1, 1) + pos];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    double lo = tb.CF[0][i] * ul;
+    if (i == 0) lo = fma(tb.CF[1][i], dl, lo);
+    y[0][i] += lo;
+    double hi = tb.CF[2][NC + i] * uh;
+    if (i == NC - 1) hi = fma(tb.CF[3][NC + i], dh, hi);
+    y[0][NC + i] += hi;
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ void lap(const double (&v)[1][NP], double (&w)[1][NP], int var) {
+  if (FAST) mv<NP, NP, LapP<0, double>, 1>(v, w);
+  else if (var == 0) mv<NP, NP, LapP<0, double>, 1>(v, w);
+  else mv<NP, NP, LapRT<double>, 1>(v, w, LapRT<double>{var});
+}
+template <bool FAST>
+__device__ __forceinline__ void lap_acc(const double (&v)[1][NP], double (&w)[1][NP], int var) {
+  if (FAST) mv_acc<NP, NP, LapP<0, double>, 1>(v, w);
+  else if (var == 0) mv_acc<NP, NP, LapP<0, double>, 1>(v, w);
+  else mv_acc<NP, NP, LapRT<double>, 1>(v, w, LapRT<double>{var});
+}
+
+struct PatchInfo {
+  int base, var[3], own;
+};
+
+template <bool FAST>
+__device__ __forceinline__ double op3_body(const double* __restrict__ x, double* __restrict__ y,
+                                           const double* __restrict__ bm, const LevelGeom& g, const PatchInfo& P,
+                                           const pair3::Deltas& dl, double* X, double* T1, const double* OWN,
+                                           double* F, bool dot) {
+  const TabData<K, double>& tb = tab<double>();
+  const int t = threadIdx.x;
+  // ---- x pass: T1 = M0 x, X = L0 x + x-normal family; the z-normal family's y mass on idle threads
+  if (t < NL) {
+    const int i1 = t % NP, i2 = t / NP;
+    const int qlo = 2 * (i1 / NC) + 4 * (i2 / NC), r0 = NC * (i1 % NC) + NC * NC * (i2 % NC);
+    double v[1][NP], w[1][NP];
+#if IPMG_OP3_STAGE_OWN
+    const double* s0 = OWN + qlo * SLOT + (int)((P.base + dl.pc[qlo]) & 1) + r0;
+    const double* s1 = OWN + (qlo + 1) * SLOT + (int)((P.base + dl.pc[qlo + 1]) & 1) + r0;
+#else
+    const double* s0 = x + (long long)(P.base + dl.pc[qlo]) * CELL + r0;
+    const double* s1 = x + (long long)(P.base + dl.pc[qlo + 1]) * CELL + r0;
+#endif
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      v[0][j] = s0[j];
+      v[0][NC + j] = s1[j];
+    }
+    mv<NP, NP, MassP<double>, 1>(v, w);
+    store_lines<NP, 1>(T1 + S1 * i1 + S2 * i2, 0, 1, w);
+    lap<FAST>(v, w, P.var[0]);
+    inject(w, F, 0, i1 + FROW * i2);
+    store_lines<NP, 1>(X + S1 * i1 + S2 * i2, 0, 1, w);
+  } else if (t - NL < 4 * NP) {
+    t2_mass(F, t - NL);
+  }
+  // lines the idle threads do not cover (k = 4: 40 lines, 28 idle threads) go to the first threads
+  if (NT - NL < 4 * NP && t < 4 * NP - (NT - NL)) t2_mass(F, NT - NL + t);
+  __syncthreads();
+  // ---- y pass: X = M1 X + L1 T1 + y-normal family, T1 = M1 T1
+  const unsigned ly = __ldg(&pair3::g_lines[0][0][t]);
+  if (ly != 0xffffffffu) {
+    const int base = (int)ly, i0 = base % S2, i2 = base / S2;
+    double m[1][NP], lx[1][NP], w[1][NP];
+    load_lines<NP, 1>(T1 + base, 0, S1, m);
+    load_lines<NP, 1>(X + base, 0, S1, lx);
+    mv<NP, NP, MassP<double>, 1>(lx, w);
+    lap_acc<FAST>(m, w, P.var[1]);
+    inject(w, F, 1, i0 + FROW * i2);
+    store_lines<NP, 1>(X + base, 0, S1, w);
+    mv<NP, NP, MassP<double>, 1>(m, w);
+    store_lines<NP, 1>(T1 + base, 0, S1, w);
+  }
+  __syncthreads();
+  // ---- z pass: y = hs (M2 X + L2 T1 + z-normal family) -> global (fused x.y)
+  double dacc = 0.0;
+  const unsigned lz = __ldg(&pair3::g_lines[0][1][t]);
+  if (lz != 0xffffffffu) {
+    const int base = (int)(lz & 0xffff), i0 = (lz >> 16) & 0xf, i1 = (lz >> 20) & 0xf;
+    double a[1][NP], bb[1][NP], w[1][NP];
+    load_lines<NP, 1>(X + base, 0, S2, a);
+    mv<NP, NP, MassP<double>, 1>(a, w);
+    load_lines<NP, 1>(T1 + base, 0, S2, bb);
+    lap_acc<FAST>(bb, w, P.var[2]);
+    inject(w, F, 2, i0 + FROW * i1);
+    const double hs = g.hs;
+    const int qb = (i0 / NC) + 2 * (i1 / NC), ob = (i0 % NC) + NC * (i1 % NC);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (!((P.own >> c) & 1)) continue;   // ghost cells of a straddling patch
+      const long long cell = (long long)P.base + dl.pc[qb + 4 * c];
+      double* yo = y + cell * CELL + ob;
+#if IPMG_OP3_STAGE_OWN
+      const double* xo = OWN + (qb + 4 * c) * SLOT + (int)(cell & 1) + ob;
+#else
+      const double* xo = x + cell * CELL + ob;
+#endif
+      const double* bo = bm ? bm + cell * CELL + ob : nullptr;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        double val = hs * w[0][c * NC + j];
+        if (bo) val = __ldg(bo + NC * NC * j) - val;
+        yo[NC * NC * j] = val;
+        if (dot) dacc = fma(xo[NC * NC * j], val, dacc);
+      }
+    }
+  }
+  return dacc;
+}
+
+#ifndef IPMG_OP3_TY
+#define IPMG_OP3_TY 8   // rows per traversal tile (as pair3: z-face neighbours stay in L2)
+#endif
+constexpr int TY = IPMG_OP3_TY;
+
+__global__ void __launch_bounds__(NT) op3_kernel(const double* __restrict__ x, double* __restrict__ y,
+                                                 const double* __restrict__ bm, LevelGeom g, int gx, int gy,
+                                                 const __grid_constant__ pair3::Deltas dl,
+                                                 double* __restrict__ dot_partial) {
+  // grid (gx, TY * gz, ceil(gy / TY)): tiles of TY patch rows, as the pair smoother
+  const int bxi = blockIdx.x, byi = (int)blockIdx.z * TY + (int)(blockIdx.y % TY), jz = (int)(blockIdx.y / TY);
+  if (byi >= gy) return;   // the last tile's missing rows (no partial: see the launcher)
+  const int bzi = g.zsel == 0 ? jz : (g.zsel == 1 ? jz + 1 : (jz == 0 ? 0 : g.znb - 1));
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* NBs = reinterpret_cast<double*>(smem_raw);
+  double* X = NBs;   // X, T1 alias the neighbour slots (dead after the trace units)
+  double* T1 = NBs + TSZ;
+  double* OWN = NBs + NNB * SLOT;   // the own cells follow the neighbour slots (slot 24 + q)
+  double* F = reinterpret_cast<double*>(smem_raw + NBB + OWNB);
+  const int t = threadIdx.x;
+  // patch data in registers (every thread: no barrier, no shared table)
+  PatchInfo P;
+  {
+    const int c0x = 2 * bxi, c0y = 2 * byi, c0z = 2 * bzi;   // colour 0: slab_first = 0
+    P.base = (int)cell_offset_cells(g, c0x, c0y, c0z);
+    const int gs = g.zoff + c0z;
+    P.own = (c0z >= 0 ? 1 : 0) | (c0z + 1 < g.n[2] ? 2 : 0);
+    P.var[0] = (c0x == 0 ? 1 : 0) | (c0x + 2 == g.n[0] ? 2 : 0);
+    P.var[1] = (c0y == 0 ? 1 : 0) | (c0y + 2 == g.n[1] ? 2 : 0);
+    P.var[2] = (gs == 0 ? 1 : 0) | (gs + 2 == g.nglob ? 2 : 0);
+  }
+  // staging: entry e < 24 the face neighbour k = e (absent across the domain boundary),
+  // e >= 24 the own cell q = e - 24, in slot e; a warp per entry.  Lane i of warp w first
+  // forms the source of entry w + NW i (one cell-index load each, in parallel), the copy
+  // loop takes them by shuffle.
+  {
+    const int lane = t & 31, w = t >> 5;
+    constexpr int NW = NT / 32, PER = (NSTAGE + NW - 1) / NW;
+    static_assert(PER <= 32, "op3 staging");
+    // an absent neighbour (face on the domain boundary) copies the patch's own first cell
+    // instead (never read: its trace units see exists = false) -- no branch in the copy loop
+    unsigned long long my = 0ull;   // 16-byte aligned source
+    {
+      const int e = w + NW * lane;
+      int cell = P.base + dl.pc[0];
+      if (lane < PER && e < NSTAGE) {
+        if (e < NNB) {
+          const int va = e < 8 ? P.var[0] : (e < 16 ? P.var[1] : P.var[2]);
+          if (!((va >> ((e >> 2) & 1)) & 1)) cell = P.base + dl.nb[e];
+        } else {
+          cell = P.base + dl.pc[e - NNB];
+        }
+      }
+      my = reinterpret_cast<unsigned long long>(x + (long long)cell * CELL) & ~15ull;
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (w + NW * i >= NSTAGE) break;
+      const unsigned long long src = __shfl_sync(0xffffffffu, my, i);
+      double* dst = NBs + (w + NW * i) * SLOT;
+      // chunks c0 + lane; lanes past the end repeat chunk CHUNKS - 1 (the same bytes): no branch
+#pragma unroll
+      for (int c0 = 0; c0 < CHUNKS; c0 += 32) {
+        const int c = c0 + lane < CHUNKS ? c0 + lane : CHUNKS - 1;
+        cp_async<16>(dst + 2 * c, reinterpret_cast<const void*>(src + 16ull * c));
+      }
+    }
+    cp_async_commit();
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // trace units: family a = u / 40, (side, t1 cell, second tangential index) within
+  if (t < 12 * NP) {
+    const int a = t / (4 * NP), r = t % (4 * NP);
+    const int ic = r % NP, h = (r / NP) & 1, s = r / (2 * NP);
+    const int tc = h + ((ic >= NC) ? 2 : 0);
+    const int k = (2 * a + s) * 4 + tc;
+    const int va = a == 0 ? P.var[0] : (a == 1 ? P.var[1] : P.var[2]);
+    const bool ex = !((va >> s) & 1);
+    const double* c = NBs + k * SLOT + (ex ? (int)((P.base + dl.nb[k]) & 1) : 0);
+    if (a == 0) trace_unit<0>(F, c, ex, s, h, ic);
+    else if (a == 1) trace_unit<1>(F, c, ex, s, h, ic);
+    else trace_unit<2>(F, c, ex, s, h, ic);
+  }
+  __syncthreads();
+  const bool fast = (P.var[0] | P.var[1] | P.var[2]) == 0;
+  const bool dot = dot_partial != nullptr;
+  double d = fast ? op3_body<true>(x, y, bm, g, P, dl, X, T1, OWN, F, dot)
+                  : op3_body<false>(x, y, bm, g, P, dl, X, T1, OWN, F, dot);
+  if (dot) {
+    // fused x.y of CG: deterministic CTA partial (fixed tree), full-grid index
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    __shared__ double wsum[NT / 32];
+    if ((t & 31) == 0) wsum[t >> 5] = d;
+    __syncthreads();
+    if (t == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += wsum[w];
+      dot_partial[bxi + (long long)gx * (byi + (long long)gy * bzi)] = s;
+    }
+  }
+}
+}  // namespace op3
+#endif

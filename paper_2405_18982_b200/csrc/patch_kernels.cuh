@@ -2179,10 +2179,62 @@ inline dim3 patch_grid(LevelGeom& g, int colour) {   // also sets g.znb (full co
   return dim3((unsigned)((m0 + C::PPC - 1) / C::PPC), (unsigned)(m1 > 0 ? m1 : 0), (unsigned)(m2 > 0 ? m2 : 0));
 }
 
+#if !IPMG_DIRICHLET
+#include "smooth_pair3.cuh"
+#include "op3.cuh"
+// 3D fp64 operator through the staged kernel (op3.cuh): bit k of IPMG_OP3_DEGREES enables
+// degree k (as measured); IPMG_OP3=0/1 in the environment forces it off / on (A/B runs)
+#ifndef IPMG_OP3_DEGREES
+#define IPMG_OP3_DEGREES 0x10
+#endif
+inline bool op3_enabled() {
+  static const int env = [] {
+    const char* e = std::getenv("IPMG_OP3");
+    return e ? std::atoi(e) : -1;
+  }();
+  return env >= 0 ? env != 0 : ((IPMG_OP3_DEGREES >> K) & 1) != 0;
+}
+inline bool op3_applies(const LevelGeom& g) {
+  return op3_enabled() && g.grouped && g.n[0] >= 2 && g.n[1] >= 2 && g.n[2] >= 2 && (g.n[0] % 2) == 0 &&
+         (g.n[1] % 2) == 0;
+}
+inline pair3::Deltas pair3_deltas(const LevelGeom& g, int colour);
+// the copies are widened to 16-byte granularity: x 16-byte aligned, and an even cell count
+// (the widened copy of the last cell ends inside the vector; ghost layers hold an even count)
+inline cudaError_t launch_op3(const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp,
+                              long long* nparts, cudaStream_t s) {
+  LevelGeom gg = g;
+  const int gx = g.n[0] / 2, gy = g.n[1] / 2;
+  int gz = slab_patches(g, 2, 0);
+  gz = gz > 0 ? gz : 0;
+  gg.znb = gz;
+  gz = slab_sel_count(gz, g.zsel);
+  if (nparts) *nparts = (long long)gx * gy * gg.znb;   // full grid
+  if (x == nullptr) return cudaSuccess;               // size query
+  if ((reinterpret_cast<unsigned long long>(x) & 15) != 0 || (g.ncells % 2) != 0) return cudaErrorNotReady;
+  cudaError_t e = set_smem(op3::op3_kernel, op3::SMEM);
+  if (e != cudaSuccess) return e;
+  if ((long long)gx * gy * gz == 0) return cudaSuccess;
+  constexpr int TY = op3::TY;
+  const dim3 grid((unsigned)gx, (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
+  op3::op3_kernel<<<grid, op3::NT, op3::SMEM, s>>>((const double*)x, (double*)y, (const double*)bm, gg, gx, gy,
+                                                  pair3_deltas(g, 0), dotp);
+  return cudaGetLastError();
+}
+#endif
+
 template <int D, typename T>
 cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp, long long* nparts,
                          cudaStream_t s) {
   using C = Cfg<D, T>;
+#if !IPMG_DIRICHLET
+  if constexpr (D == 3 && sizeof(T) == 8) {
+    if (op3_applies(g)) {
+      const cudaError_t e = launch_op3(x, y, g, bm, dotp, nparts, s);
+      if (e != cudaErrorNotReady) return e;
+    }
+  }
+#endif
   LevelGeom gg = g;
   const dim3 grid = patch_grid<D, T>(gg, 0);
   if (nparts) *nparts = (long long)grid.x * (D == 3 ? (long long)grid.y * gg.znb : gg.znb);   // full grid
@@ -2196,7 +2248,6 @@ cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void*
 }
 
 #if !IPMG_DIRICHLET
-#include "smooth_pair3.cuh"
 // 3D fp32 colour passes through the patch-pair kernel (smooth_pair3.cuh): bit k of
 // IPMG_PAIR3_DEGREES enables degree k (as measured); IPMG_PAIR3=0/1 in the
 // environment forces it off / on for every degree (A/B runs)
