@@ -34,6 +34,10 @@ namespace pair3 {
                               // 78 instead of 82 registers, 6 CTAs/SM; 3D k=4 colour pass 1.65 -> 1.60 ms
 #endif
 
+#ifndef IPMG_PAIR3_SHFLSTAGE
+#define IPMG_PAIR3_SHFLSTAGE 1   // 1: staging sources formed in parallel by the lanes, taken by shuffle,
+                                 // branch-free copies, no shared table or barrier before the copies
+#endif
 constexpr int NL = NP * NP;               // lines per direction per patch
 constexpr int CELL = NC * NC * NC;
 constexpr int H = NP / 2;
@@ -486,7 +490,9 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
   float2* F = reinterpret_cast<float2*>(smem_raw + (C::XB > C::NBB ? C::XB : C::NBB));
   __shared__ Pat<NPAT> P;
   __shared__ __align__(16) float zslot[CELL];   // read by the trace units of a missing neighbour
+#if !IPMG_PAIR3_SHFLSTAGE
   __shared__ unsigned long long nba[NPAT * NNB];  // 16-byte aligned source of each staged cell, 0: none
+#endif
   const int t = threadIdx.x;
   for (int e = t; e < CELL; e += C::NT) zslot[e] = 0.f;
   // y / z line of this thread (host tables)
@@ -494,6 +500,81 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
   const int ybase = ly == 0xffffffffu ? -1 : (int)ly;
   const int zbase = lz == 0xffffffffu ? -1 : (int)(lz & 0xffff);
   const int zm0 = (lz >> 16) & 0xf, zm1 = (lz >> 20) & 0xf, zq = (lz >> 24) & 0xf;
+#if IPMG_PAIR3_SHFLSTAGE
+  // patch data of the CTA (x-blocks of NPAT patches, row by, plane bz) in registers of
+  // every thread; threads p < NPAT also write the shared copy P, read only after the
+  // barrier that opens the trace phase
+  int pbase[NPAT], pvalid[NPAT], pvar[NPAT][3];
+#pragma unroll
+  for (int p = 0; p < NPAT; ++p) {
+    const int m0 = g.n[0] / 2 - (colour & 1);
+    const int c0y = ((colour >> 1) & 1) + 2 * byi;
+    const int c0z = slab_first(g, (colour >> 2) & 1) + 2 * bzi;
+    const int j0 = bxi * NPAT + p;
+    const bool valid = j0 < m0;
+    const int c0x = (colour & 1) + 2 * (valid ? j0 : 0);
+    pbase[p] = (int)cell_offset_cells(g, c0x, c0y, c0z);
+    pvalid[p] = valid;
+    const int gs = g.zoff + c0z;
+    pvar[p][0] = (c0x == 0 ? 1 : 0) | (c0x + 2 == g.n[0] ? 2 : 0);
+    pvar[p][1] = (c0y == 0 ? 1 : 0) | (c0y + 2 == g.n[1] ? 2 : 0);
+    pvar[p][2] = (gs == 0 ? 1 : 0) | (gs + 2 == g.nglob ? 2 : 0);
+    if (t == p) {
+      P.base[p] = pbase[p];
+      P.valid[p] = pvalid[p];
+      P.own[p] = (c0z >= 0 ? 1 : 0) | (c0z + 1 < g.n[2] ? 2 : 0);
+      P.var[p][0] = pvar[p][0];
+      P.var[p][1] = pvar[p][1];
+      P.var[p][2] = pvar[p][2];
+    }
+  }
+  if (x_in != nullptr) {
+    // face-neighbour cells -> shared memory: 16-byte cp.async, a warp per cell (lanes on
+    // consecutive chunks), each copy widened to the 16-byte boundaries around the cell
+    // (inside the vector: its base and end are 16-byte aligned, checked by the launcher).
+    // Lane i of warp w first forms the source of entry w + NW i (in parallel); the copy
+    // loop takes it by shuffle.  A missing neighbour copies the patch's first cell instead
+    // (its trace units read the zero slot): no branch in the copy loop.
+    const int lane = t & 31, w = t >> 5;
+    constexpr int NW = C::NT / 32, PER = (NPAT * NNB + NW - 1) / NW;
+    constexpr int NR = (PER + 31) / 32;   // rounds of 32 entries per warp
+    constexpr int CMIN = (CELL * 4 + 15) / 16;   // chunks of a cell at a 16-byte boundary; one more otherwise
+    unsigned long long my[NR];   // 16-byte aligned source | (chunk count - CMIN)
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+      const int e = w + NW * (32 * rr + lane);
+      const int p = e / NNB, k = e - NNB * (e / NNB);
+      int cell = pbase[0];
+      if (32 * rr + lane < PER && e < NPAT * NNB) {
+        int pb = pbase[0], pv = pvalid[0], va = pvar[0][0], vb = pvar[0][1], vc = pvar[0][2];
+#pragma unroll
+        for (int pp = 1; pp < NPAT; ++pp)
+          if (p == pp) { pb = pbase[pp]; pv = pvalid[pp]; va = pvar[pp][0]; vb = pvar[pp][1]; vc = pvar[pp][2]; }
+        const int vk = (k >> 3) == 0 ? va : ((k >> 3) == 1 ? vb : vc);
+        if (pv && !((vk >> ((k >> 2) & 1)) & 1)) cell = pb + dl.nb[k];
+      }
+      const unsigned long long a0 = reinterpret_cast<unsigned long long>(x_in + (long long)cell * CELL);
+      const unsigned chunks = (CELL * 4 + 4 * (unsigned)((a0 >> 2) & 3) + 15) / 16;
+      my[rr] = (a0 & ~15ull) | (unsigned long long)(chunks - CMIN);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (w + NW * i >= NPAT * NNB) break;
+      const unsigned long long ent = __shfl_sync(0xffffffffu, my[i / 32], i % 32);
+      const unsigned long long src = ent & ~15ull;
+      const int last = CMIN - 1 + (int)(ent & 15ull);   // the cell's last chunk
+      float* dst = NBs + (w + NW * i) * SLOTF;
+#pragma unroll
+      for (int c0 = 0; c0 < (CELL * 4 + 12 + 15) / 16; c0 += 32) {   // the most chunks a cell can need
+        const int c = c0 + lane < last ? c0 + lane : last;   // lanes past the end repeat the last chunk
+        cp_async<16>(dst + 4 * c, reinterpret_cast<const void*>(src + 16ull * c));
+      }
+    }
+    cp_async_commit();
+  } else {
+    __syncthreads();   // P before the x pass (no trace phase)
+  }
+#else
   // patches of the CTA (x-blocks of NPAT patches, row by, plane bz)
   if (t < NPAT) {
     const int p = t;
@@ -546,6 +627,7 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
     }
     cp_async_commit();
   }
+#endif
   // b rows of this thread's x-line pair (in flight during the trace phase)
   float2 brow[NP];
   {
@@ -556,7 +638,11 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
   bool allint = true;
 #pragma unroll
   for (int p = 0; p < NPAT; ++p)
+#if IPMG_PAIR3_SHFLSTAGE
+    if (pvalid[p] && (pvar[p][0] | pvar[p][1] | pvar[p][2])) allint = false;
+#else
     if (P.valid[p] && (P.var[p][0] | P.var[p][1] | P.var[p][2])) allint = false;
+#endif
   if (allint)
     pair_body<NPAIR, true>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0, zm1);
   else
