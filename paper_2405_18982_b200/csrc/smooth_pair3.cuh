@@ -38,6 +38,12 @@ namespace pair3 {
 #define IPMG_PAIR3_SHFLSTAGE 1   // 1: staging sources formed in parallel by the lanes, taken by shuffle,
                                  // branch-free copies, no shared table or barrier before the copies
 #endif
+#ifndef IPMG_PAIR3_STASM
+#define IPMG_PAIR3_STASM 1   // 1: pair stores to shared memory as st.shared.v2.f32 inline asm (see sts2)
+#endif
+#ifndef IPMG_PAIR3_BPF
+#define IPMG_PAIR3_BPF 2   // 1: L1 prefetch of the b cells at the start (SHFLSTAGE path)
+#endif
 constexpr int NL = NP * NP;               // lines per direction per patch
 constexpr int CELL = NC * NC * NC;
 constexpr int H = NP / 2;
@@ -182,9 +188,20 @@ __device__ __forceinline__ void ld_line(const float2* X, int base, int stride, f
 #pragma unroll
   for (int j = 0; j < NP; ++j) v[j] = X[base + j * stride];
 }
+// shared-memory store of a pair: as inline st.shared.v2.f32 ptxas keeps the value in the
+// registers the FFMA2 wrote (a plain float2 store got two MOVs into a staging pair before
+// almost every STS.64: 3D k=4 colour pass 1.575 -> 1.528 ms)
+__device__ __forceinline__ void sts2(float2* p, float2 v) {
+#if IPMG_PAIR3_STASM
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"((unsigned)__cvta_generic_to_shared(p)), "f"(v.x), "f"(v.y)
+               : "memory");
+#else
+  *p = v;
+#endif
+}
 __device__ __forceinline__ void st_line(float2* X, int base, int stride, const float2 (&v)[NP]) {
 #pragma unroll
-  for (int j = 0; j < NP; ++j) X[base + j * stride] = v[j];
+  for (int j = 0; j < NP; ++j) sts2(X + base + j * stride, v[j]);
 }
 
 // one pair row of b (scaled) from global: row (i1, i2) of both patches, zeros for an invalid patch
@@ -290,8 +307,8 @@ __device__ __forceinline__ void trace_unit(float2* F, const float* NBs, const fl
       mu = fma2(tb.M[lb][i], u[lb], mu);
       md = fma2(tb.M[lb][i], du[lb], md);
     }
-    fu[i] = mu;
-    fd[i] = md;
+    sts2(fu + i, mu);
+    sts2(fd + i, md);
   }
 }
 
@@ -528,6 +545,26 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
       P.var[p][2] = pvar[p][2];
     }
   }
+#if IPMG_PAIR3_BPF
+  // L1 prefetch of the b cells of the CTA's patches (read by the x pass; no registers held
+  // meanwhile): thread t < 16 NPAIR * BL covers line t % BL of cell t / BL
+  {
+    constexpr int BL = (CELL * 4 + 127 + 124) / 128;   // lines a cell can touch
+    if (t < NPAT * 8 * BL) {
+      const int ce = t / BL, ln = t % BL, p = ce >> 3, q = ce & 7;
+      int pb = pbase[0], pv = pvalid[0];
+#pragma unroll
+      for (int pp = 1; pp < NPAT; ++pp)
+        if (p == pp) { pb = pbase[pp]; pv = pvalid[pp]; }
+      const unsigned long long c0 = reinterpret_cast<unsigned long long>(b + (long long)(pb + dl.pc[q]) * CELL);
+      const unsigned long long a = (c0 & ~127ull) + 128ull * ln;
+      if (pv && a < c0 + CELL * 4) {
+        if (IPMG_PAIR3_BPF == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+        else asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a));
+      }
+    }
+  }
+#endif
   if (x_in != nullptr) {
     // face-neighbour cells -> shared memory: 16-byte cp.async, a warp per cell (lanes on
     // consecutive chunks), each copy widened to the 16-byte boundaries around the cell
