@@ -2338,7 +2338,8 @@ cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const L
   if (e != cudaSuccess) return e;
   constexpr int TY = pair3::TY;
   const dim3 grid((unsigned)(gx + (colour != 0 && g.zsel != 2 ? 1 : 0)), (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
-  pair3::smooth_pair3_kernel<NPAIR><<<grid, C::NT, C::SMEM, s>>>((const float*)xi, (const float*)b, (float*)xo, gg,
+  // a zero-start pass (xi == nullptr) has no neighbour staging and no face arrays: X only
+  pair3::smooth_pair3_kernel<NPAIR><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>((const float*)xi, (const float*)b, (float*)xo, gg,
                                                                colour, gx, gy, pair3_deltas(g, colour));
   return cudaGetLastError();
 }
@@ -2353,8 +2354,11 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
   // (zero-start passes, x_in == nullptr, stay on smooth_kernel: without face traces the
   // pair kernel's fewer instructions do not make up for its lower occupancy, measured
   // 3D k=4 colour 0 from zero 0.84 vs 0.94 ms)
-  if (D == 3 && sizeof(T) == 4 && xi != nullptr && pair3_enabled() && g.grouped && g.n[0] >= 2 && g.n[1] >= 2 &&
-      g.n[2] >= 2 &&
+#ifndef IPMG_PAIR3_ZERO
+#define IPMG_PAIR3_ZERO 0   // 1: zero-start passes (x_in == nullptr) through the pair kernel too
+#endif
+  if (D == 3 && sizeof(T) == 4 && (xi != nullptr || IPMG_PAIR3_ZERO) && pair3_enabled() && g.grouped &&
+      g.n[0] >= 2 && g.n[1] >= 2 && g.n[2] >= 2 &&
       (reinterpret_cast<unsigned long long>(xi) & 15) == 0 && (g.ncells % 4) == 0 &&
       (reinterpret_cast<unsigned long long>(xo) & 3) == 0) {
     const cudaError_t e = launch_smooth_pair3<IPMG_PAIR3_NPAIR>(xi, b, xo, g, colour, s);
