@@ -56,6 +56,9 @@ constexpr size_t SMEM = NBB + OWNB + FB;
 static_assert(XB <= NBB, "op3: X, T1 alias the neighbour slots");
 
 __device__ __forceinline__ int farr(int a, int s, int kind) { return ((a * 2 + s) * 2 + kind) * FARR; }
+// doubles between a staged cell's slot start and the cell: 1 when the cell starts 8 bytes
+// past a 16-byte boundary (odd cell index and odd CELL; x is 16-byte aligned)
+__device__ __forceinline__ int soff(long long cell) { return (int)(cell & (long long)(CELL & 1)); }
 
 // Trace unit of family A (compile-time: one code path per family, no selects):
 // u[lb] = x(face node), du[lb] = sum_j phi_j'(face) x_j of the neighbour across face
@@ -170,8 +173,8 @@ __device__ __forceinline__ double op3_body(const double* __restrict__ x, double*
     const int qlo = 2 * (i1 / NC) + 4 * (i2 / NC), r0 = NC * (i1 % NC) + NC * NC * (i2 % NC);
     double v[1][NP], w[1][NP];
 #if IPMG_OP3_STAGE_OWN
-    const double* s0 = OWN + qlo * SLOT + (int)((P.base + dl.pc[qlo]) & 1) + r0;
-    const double* s1 = OWN + (qlo + 1) * SLOT + (int)((P.base + dl.pc[qlo + 1]) & 1) + r0;
+    const double* s0 = OWN + qlo * SLOT + soff(P.base + dl.pc[qlo]) + r0;
+    const double* s1 = OWN + (qlo + 1) * SLOT + soff(P.base + dl.pc[qlo + 1]) + r0;
 #else
     const double* s0 = x + (long long)(P.base + dl.pc[qlo]) * CELL + r0;
     const double* s1 = x + (long long)(P.base + dl.pc[qlo + 1]) * CELL + r0;
@@ -226,7 +229,7 @@ __device__ __forceinline__ double op3_body(const double* __restrict__ x, double*
       const long long cell = (long long)P.base + dl.pc[qb + 4 * c];
       double* yo = y + cell * CELL + ob;
 #if IPMG_OP3_STAGE_OWN
-      const double* xo = OWN + (qb + 4 * c) * SLOT + (int)(cell & 1) + ob;
+      const double* xo = OWN + (qb + 4 * c) * SLOT + soff(cell) + ob;
 #else
       const double* xo = x + cell * CELL + ob;
 #endif
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(NT) op3_kernel(const double* __restrict__ x, d
     const int k = (2 * a + s) * 4 + tc;
     const int va = a == 0 ? P.var[0] : (a == 1 ? P.var[1] : P.var[2]);
     const bool ex = !((va >> s) & 1);
-    const double* c = NBs + k * SLOT + (ex ? (int)((P.base + dl.nb[k]) & 1) : 0);
+    const double* c = NBs + k * SLOT + (ex ? soff(P.base + dl.nb[k]) : 0);
     if (a == 0) trace_unit<0>(F, c, ex, s, h, ic);
     else if (a == 1) trace_unit<1>(F, c, ex, s, h, ic);
     else trace_unit<2>(F, c, ex, s, h, ic);

@@ -2185,7 +2185,7 @@ inline dim3 patch_grid(LevelGeom& g, int colour) {   // also sets g.znb (full co
 // 3D fp64 operator through the staged kernel (op3.cuh): bit k of IPMG_OP3_DEGREES enables
 // degree k (as measured); IPMG_OP3=0/1 in the environment forces it off / on (A/B runs)
 #ifndef IPMG_OP3_DEGREES
-#define IPMG_OP3_DEGREES 0x10
+#define IPMG_OP3_DEGREES 0x7c   // k = 2..6 (tools/gpu_deg_ab.sh: k = 7 slower, 2.30 vs 1.68 ms)
 #endif
 inline bool op3_enabled() {
   static const int env = [] {
@@ -2252,7 +2252,7 @@ cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void*
 // IPMG_PAIR3_DEGREES enables degree k (as measured); IPMG_PAIR3=0/1 in the
 // environment forces it off / on for every degree (A/B runs)
 #ifndef IPMG_PAIR3_DEGREES
-#define IPMG_PAIR3_DEGREES 0x10
+#define IPMG_PAIR3_DEGREES 0x54   // k = 2, 4, 6 (tools/gpu_deg_ab.sh: k = 3, 5, 7 slower)
 #endif
 #ifndef IPMG_PAIR3_NPAIR
 #define IPMG_PAIR3_NPAIR 1
