@@ -34,10 +34,6 @@ namespace pair3 {
                               // 78 instead of 82 registers, 6 CTAs/SM; 3D k=4 colour pass 1.65 -> 1.60 ms
 #endif
 
-#ifndef IPMG_PAIR3_SPLIT
-#define IPMG_PAIR3_SPLIT 0   // 1: stage the x/y-normal neighbour cells first and the z-normal ones in a
-                             // second round into the x-normal slots (2/3 of the staging memory)
-#endif
 #ifndef IPMG_PAIR3_SHFLSTAGE
 #define IPMG_PAIR3_SHFLSTAGE 1   // 1: staging sources formed in parallel by the lanes, taken by shuffle,
                                  // branch-free copies, no shared table or barrier before the copies
@@ -79,7 +75,7 @@ struct PC {
   static constexpr int UNITS = NPAIR * 6 * 2 * NP;       // trace units: (pair, a, side, h, ic)
   static constexpr int FLINES = NPAIR * 12 * NP;         // second-tangential mass lines
   static constexpr size_t XB = sizeof(float2) * (size_t)NPAIR * TSZ;
-  static constexpr size_t NBB = sizeof(float) * (size_t)NPAT * (IPMG_PAIR3_SPLIT ? 16 : NNB) * SLOTF;
+  static constexpr size_t NBB = sizeof(float) * (size_t)NPAT * NNB * SLOTF;
   static constexpr size_t FB = sizeof(float2) * (size_t)NPAIR * FPAIR;
   // X aliases the neighbour staging (dead after the trace phase)
   static constexpr size_t SMEM = (XB > NBB ? XB : NBB) + FB;
@@ -181,11 +177,6 @@ struct Deltas {
   int pc[8];
   int nb[NNB];
 };
-// staging slot of face neighbour k of patch p (split staging: the z-normal cells k >= 16
-// reuse the x-normal slots k - 16 in the second round)
-__device__ __forceinline__ int slot_of(int p, int k) {
-  return IPMG_PAIR3_SPLIT ? p * 16 + (k & 15) : p * NNB + k;
-}
 // face neighbour k of patch p exists (and is staged) iff its face is not on the domain boundary
 template <int NPAT>
 __device__ __forceinline__ bool nb_exists(const Pat<NPAT>& P, int p, int k) {
@@ -278,7 +269,7 @@ __device__ __forceinline__ void trace_unit(float2* F, const float* NBs, const fl
   for (int pp = 0; pp < 2; ++pp) {
     const int p = 2 * q + pp;
     c[pp] = nb_exists(P, p, k)
-                ? NBs + slot_of(p, k) * SLOTF + (int)(((long long)(P.base[p] + dl.nb[k]) * CELL) & 3) + lc * Rl
+                ? NBs + (p * NNB + k) * SLOTF + (int)(((long long)(P.base[p] + dl.nb[k]) * CELL) & 3) + lc * Rl
                 : zslot;
   }
   float2 v[NC][NC];   // [row][column]
@@ -321,88 +312,6 @@ __device__ __forceinline__ void trace_unit(float2* F, const float* NBs, const fl
   }
 }
 
-// Face-neighbour cells k = K0 .. K0 + NK - 1 of the CTA's patches -> their staging slots:
-// 16-byte cp.async, a warp per cell (lanes on consecutive chunks), each copy widened to the
-// 16-byte boundaries around the cell (inside the vector: its base and end are 16-byte
-// aligned, checked by the launcher).  Lane i of warp w first forms the source of entry
-// w + NW i (in parallel); the copy loop takes it by shuffle.  A missing neighbour copies
-// the patch's first cell instead (its trace units read the zero slot): no branch.
-template <int NPAT, int NT, int K0, int NK>
-__device__ __forceinline__ void stage_cells(const float* __restrict__ x_in, float* NBs, const Deltas& dl,
-                                            const int (&pbase)[NPAT], const int (&pvalid)[NPAT],
-                                            const int (&pvar)[NPAT][3]) {
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  constexpr int NE = NPAT * NK, NW = NT / 32, PER = (NE + NW - 1) / NW;
-  constexpr int NR = (PER + 31) / 32;          // rounds of 32 entries per warp
-  constexpr int CMIN = (CELL * 4 + 15) / 16;   // chunks of a cell at a 16-byte boundary; one more otherwise
-  unsigned long long my[NR];                   // 16-byte aligned source | (chunk count - CMIN)
-#pragma unroll
-  for (int rr = 0; rr < NR; ++rr) {
-    const int e = w + NW * (32 * rr + lane);
-    const int p = e / NK, k = K0 + e - NK * (e / NK);
-    int cell = pbase[0];
-    if (32 * rr + lane < PER && e < NE) {
-      int pb = pbase[0], pv = pvalid[0], va = pvar[0][0], vb = pvar[0][1], vc = pvar[0][2];
-#pragma unroll
-      for (int pp = 1; pp < NPAT; ++pp)
-        if (p == pp) { pb = pbase[pp]; pv = pvalid[pp]; va = pvar[pp][0]; vb = pvar[pp][1]; vc = pvar[pp][2]; }
-      const int vk = (k >> 3) == 0 ? va : ((k >> 3) == 1 ? vb : vc);
-      if (pv && !((vk >> ((k >> 2) & 1)) & 1)) cell = pb + dl.nb[k];
-    }
-    const unsigned long long a0 = reinterpret_cast<unsigned long long>(x_in + (long long)cell * CELL);
-    const unsigned chunks = (CELL * 4 + 4 * (unsigned)((a0 >> 2) & 3) + 15) / 16;
-    my[rr] = (a0 & ~15ull) | (unsigned long long)(chunks - CMIN);
-  }
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int e = w + NW * i;
-    if (e >= NE) break;
-    const unsigned long long ent = __shfl_sync(0xffffffffu, my[i / 32], i % 32);
-    const unsigned long long src = ent & ~15ull;
-    const int last = CMIN - 1 + (int)(ent & 15ull);   // the cell's last chunk
-    const int p = e / NK, k = K0 + e - NK * (e / NK);
-    float* dst = NBs + slot_of(p, k) * SLOTF;
-#pragma unroll
-    for (int c0 = 0; c0 < (CELL * 4 + 12 + 15) / 16; c0 += 32) {   // the most chunks a cell can need
-      const int c = c0 + lane < last ? c0 + lane : last;   // lanes past the end repeat the last chunk
-      cp_async<16>(dst + 4 * c, reinterpret_cast<const void*>(src + 16ull * c));
-    }
-  }
-}
-
-// tangential cell mass along t2 (block diagonal) on the (u, u') array pair of line o of
-// (family, side) fs of pair q; the u' array is replaced by the combination the boundary row
-// of the x pass needs, V = CF_u(ib) u + CF_u'(ib) u' (ib: the outermost node on the side),
-// so the injection reads one array per family without branches
-__device__ __forceinline__ void t2_line(float2* F, int q, int fs, int o) {
-  const TabData<K, float>& tb = c_tab32;
-  const int sd = fs & 1;
-  float2* bu = F + q * FPAIR + (2 * fs) * FARR + o;
-  float2* bd = bu + FARR;
-  float2 v[NP], w[NP], dv[NP], dw[NP];
-  ld_line(bu, 0, FROW, v);
-  ld_line(bd, 0, FROW, dv);
-#pragma unroll
-  for (int c = 0; c < 2; ++c)
-#pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      float2 acc = make_float2(0.f, 0.f), dacc = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        acc = fma2(tb.M[j][i], v[c * NC + j], acc);
-        dacc = fma2(tb.M[j][i], dv[c * NC + j], dacc);
-      }
-      w[c * NC + i] = acc;
-      dw[c * NC + i] = dacc;
-    }
-  const float cu = sd == 0 ? tb.CF[0][0] : tb.CF[2][NP - 1];
-  const float cd = sd == 0 ? tb.CF[1][0] : tb.CF[3][NP - 1];
-#pragma unroll
-  for (int j = 0; j < NP; ++j) dw[j] = fma2(cd, dw[j], mul2(w[j], f2(cu)));
-  st_line(bu, 0, FROW, w);
-  st_line(bd, 0, FROW, dw);
-}
-
 // the pair kernel; FAST: every valid patch of the CTA is interior (variant 0 in all
 // directions) -> even/odd factors with compile-time constants
 template <int NPAIR, bool FAST>
@@ -418,50 +327,46 @@ __device__ __forceinline__ void pair_body(const float* __restrict__ x_in, const 
   if (faces) {
     cp_async_wait_all();
     __syncthreads();
-#if IPMG_PAIR3_SPLIT
-    // round 1: x- and y-normal families (their cells were staged at the start)
-    for (int u = t; u < NPAIR * 4 * 2 * NP; u += C::NT) {
-      const int q = u / (4 * 2 * NP), r = u % (4 * 2 * NP), a = r / (4 * NP), w = r % (4 * NP);
-      const int ic = w % NP, h = (w / NP) & 1, s = w / (2 * NP);
-      trace_unit(F, NBs, zslot, P, dl, q, a, s, h, ic);
-    }
-    __syncthreads();
-    {
-      // round 2: the z-normal cells into the x-normal slots, in flight during the t2 pass
-      // of the first two families
-      int pbase[2 * NPAIR], pvalid[2 * NPAIR], pvar[2 * NPAIR][3];
-#pragma unroll
-      for (int p = 0; p < 2 * NPAIR; ++p) {
-        pbase[p] = P.base[p];
-        pvalid[p] = P.valid[p];
-        pvar[p][0] = P.var[p][0];
-        pvar[p][1] = P.var[p][1];
-        pvar[p][2] = P.var[p][2];
-      }
-      stage_cells<2 * NPAIR, C::NT, 16, 8>(x_in, const_cast<float*>(NBs), dl, pbase, pvalid, pvar);
-      cp_async_commit();
-    }
-    for (int e = t; e < NPAIR * 4 * NP; e += C::NT) t2_line(F, e / (4 * NP), (e % (4 * NP)) / NP, e % NP);
-    cp_async_wait_all();
-    __syncthreads();
-    for (int u = t; u < NPAIR * 2 * 2 * NP; u += C::NT) {
-      const int q = u / (2 * 2 * NP), w = u % (2 * 2 * NP);
-      const int ic = w % NP, h = (w / NP) & 1, s = w / (2 * NP);
-      trace_unit(F, NBs, zslot, P, dl, q, 2, s, h, ic);
-    }
-    __syncthreads();
-    for (int e = t; e < NPAIR * 2 * NP; e += C::NT) t2_line(F, e / (2 * NP), 4 + (e % (2 * NP)) / NP, e % NP);
-    __syncthreads();
-#else
     for (int u = t; u < C::UNITS; u += C::NT) {
       const int q = u / (6 * 2 * NP), r = u % (6 * 2 * NP), a = r / (4 * NP), w = r % (4 * NP);
       const int ic = w % NP, h = (w / NP) & 1, s = w / (2 * NP);
       trace_unit(F, NBs, zslot, P, dl, q, a, s, h, ic);
     }
     __syncthreads();
-    for (int e = t; e < C::FLINES / 2; e += C::NT) t2_line(F, e / (6 * NP), (e % (6 * NP)) / NP, e % NP);
+    // tangential cell mass along t2 (block diagonal) on the (u, u') array pair of every
+    // (family, side) line; the u' array is replaced by the combination the boundary row
+    // of the x pass needs, V = CF_u(ib) u + CF_u'(ib) u' (ib: the outermost node on the
+    // side), so the injection reads one array per family without branches
+    for (int e = t; e < C::FLINES / 2; e += C::NT) {
+      const int q = e / (6 * NP), r = e % (6 * NP), fs = r / NP, o = r % NP;
+      const int sd = fs & 1, ib = sd == 0 ? 0 : NP - 1;
+      float2* bu = F + q * FPAIR + (2 * fs) * FARR + o;
+      float2* bd = bu + FARR;
+      float2 v[NP], w[NP], dv[NP], dw[NP];
+      ld_line(bu, 0, FROW, v);
+      ld_line(bd, 0, FROW, dv);
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          float2 acc = make_float2(0.f, 0.f), dacc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < NC; ++j) {
+            acc = fma2(tb.M[j][i], v[c * NC + j], acc);
+            dacc = fma2(tb.M[j][i], dv[c * NC + j], dacc);
+          }
+          w[c * NC + i] = acc;
+          dw[c * NC + i] = dacc;
+        }
+      const float cu = sd == 0 ? tb.CF[0][0] : tb.CF[2][NP - 1];
+      const float cd = sd == 0 ? tb.CF[1][0] : tb.CF[3][NP - 1];
+      (void)ib;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) dw[j] = fma2(cd, dw[j], mul2(w[j], f2(cu)));
+      st_line(bu, 0, FROW, w);
+      st_line(bd, 0, FROW, dw);
+    }
     __syncthreads();
-#endif
   }
   // ---- x pass: rhs rows (h^{2-d} b - C x_ext), S_x^T
   const int q0 = t / NL, l0 = t % NL;
@@ -667,7 +572,41 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
     // Lane i of warp w first forms the source of entry w + NW i (in parallel); the copy
     // loop takes it by shuffle.  A missing neighbour copies the patch's first cell instead
     // (its trace units read the zero slot): no branch in the copy loop.
-    stage_cells<NPAT, C::NT, 0, IPMG_PAIR3_SPLIT ? 16 : NNB>(x_in, NBs, dl, pbase, pvalid, pvar);
+    const int lane = t & 31, w = t >> 5;
+    constexpr int NW = C::NT / 32, PER = (NPAT * NNB + NW - 1) / NW;
+    constexpr int NR = (PER + 31) / 32;   // rounds of 32 entries per warp
+    constexpr int CMIN = (CELL * 4 + 15) / 16;   // chunks of a cell at a 16-byte boundary; one more otherwise
+    unsigned long long my[NR];   // 16-byte aligned source | (chunk count - CMIN)
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+      const int e = w + NW * (32 * rr + lane);
+      const int p = e / NNB, k = e - NNB * (e / NNB);
+      int cell = pbase[0];
+      if (32 * rr + lane < PER && e < NPAT * NNB) {
+        int pb = pbase[0], pv = pvalid[0], va = pvar[0][0], vb = pvar[0][1], vc = pvar[0][2];
+#pragma unroll
+        for (int pp = 1; pp < NPAT; ++pp)
+          if (p == pp) { pb = pbase[pp]; pv = pvalid[pp]; va = pvar[pp][0]; vb = pvar[pp][1]; vc = pvar[pp][2]; }
+        const int vk = (k >> 3) == 0 ? va : ((k >> 3) == 1 ? vb : vc);
+        if (pv && !((vk >> ((k >> 2) & 1)) & 1)) cell = pb + dl.nb[k];
+      }
+      const unsigned long long a0 = reinterpret_cast<unsigned long long>(x_in + (long long)cell * CELL);
+      const unsigned chunks = (CELL * 4 + 4 * (unsigned)((a0 >> 2) & 3) + 15) / 16;
+      my[rr] = (a0 & ~15ull) | (unsigned long long)(chunks - CMIN);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (w + NW * i >= NPAT * NNB) break;
+      const unsigned long long ent = __shfl_sync(0xffffffffu, my[i / 32], i % 32);
+      const unsigned long long src = ent & ~15ull;
+      const int last = CMIN - 1 + (int)(ent & 15ull);   // the cell's last chunk
+      float* dst = NBs + (w + NW * i) * SLOTF;
+#pragma unroll
+      for (int c0 = 0; c0 < (CELL * 4 + 12 + 15) / 16; c0 += 32) {   // the most chunks a cell can need
+        const int c = c0 + lane < last ? c0 + lane : last;   // lanes past the end repeat the last chunk
+        cp_async<16>(dst + 4 * c, reinterpret_cast<const void*>(src + 16ull * c));
+      }
+    }
     cp_async_commit();
   } else {
     __syncthreads();   // P before the x pass (no trace phase)
