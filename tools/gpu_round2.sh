@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
   --csv --log-file gpurun_out/launches_${TAG}.csv python profiles/solve_once.py > gpurun_out/launches_${TAG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:smooth_pair3 -s 0 -c 2 \
   -o gpurun_out/prof_smooth_${TAG} -f python profiles/solve_once.py > gpurun_out/prof_smooth_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:vmult_kernel -s 0 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"op3_kernel|vmult_kernel" -s 0 -c 1 \
   -o gpurun_out/prof_vmult_${TAG} -f python profiles/solve_once.py > gpurun_out/prof_vmult_${TAG}.log 2>&1
 fi
 ls -la gpurun_out
