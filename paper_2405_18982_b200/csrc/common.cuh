@@ -99,6 +99,11 @@ struct KernelSet {
                        const void* b_minus, double* dotp, long long* nparts, cudaStream_t s);
   cudaError_t (*smooth)(int dim, int prec, const void* x_in, const void* b, void* x_out,
                         const LevelGeom& g, int colour, cudaStream_t s);
+  // the same pass with the mixed PCG's r.z fused (partials into dotp, *nparts their count;
+  // *nparts = 0: not fused, the caller forms the dot); nullptr in the Dirichlet kernel sets
+  cudaError_t (*smooth_rz)(int dim, int prec, const void* x_in, const void* b, void* x_out,
+                           const LevelGeom& g, int colour, const double* r, double* dotp, long long* nparts,
+                           cudaStream_t s);
   cudaError_t (*additive)(int dim, int prec, const void* r, void* x, const LevelGeom& g, int colour,
                           double omega, cudaStream_t s);
   cudaError_t (*restrict_)(int dim, int prec, const void* x, const void* b, void* rc,

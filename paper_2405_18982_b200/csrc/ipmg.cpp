@@ -288,6 +288,11 @@ struct ipmg_handle {
   }
 
   // ------------------------------------------------------------ building blocks
+  // r.z fused into the V-cycle's last finest-level colour pass (mixed PCG): set by the
+  // solver around vcycle_level(L); rz_nparts > 0 afterwards when the pass could fuse it
+  const double* rz_r = nullptr;
+  double* rz_part = nullptr;
+  long long rz_nparts = 0;
   ipmg_status smooth_colour(int level, int prec, const void* xi, const void* b, void* xo, int colour) {
     return run(KC_SMOOTH, level, smooth_bytes(level, prec, colour, xi != nullptr), 1,
                [&] {
@@ -312,7 +317,18 @@ struct ipmg_handle {
       const int c = reverse ? ncol - 1 - i : i;
       const bool zero = i == 0 && x_is_zero;
       // every colour with x reads face traces (and straddling cells) of the neighbour slabs
-      ipmg_status st = zero ? smooth_colour(level, prec, nullptr, b, nxt, c) : smooth_colour_halo(level, prec, cur, b, nxt, c);
+      ipmg_status st;
+      if (!zero && rz_r && i == ncol - 1 && level == nlev - 1 && cfg.kernel == IPMG_KERNEL_FULL && ks.smooth_rz) {
+        long long np = 0;
+        st = halo_then(level, prec, cur, KC_SMOOTH, smooth_bytes(level, prec, c, true) + 8.0 * ndofs[level],
+                       [&](const ipmg::LevelGeom& g) {
+                         return ks.smooth_rz(dim, prec, cur, b, nxt, g, c, rz_r, rz_part, &np, stream);
+                       },
+                       "smooth_colour");
+        rz_nparts = np;
+      } else {
+        st = zero ? smooth_colour(level, prec, nullptr, b, nxt, c) : smooth_colour_halo(level, prec, cur, b, nxt, c);
+      }
       if (st != IPMG_OK) return st;
       std::swap(cur, nxt);
     }
@@ -436,6 +452,21 @@ struct ipmg_handle {
     }
     n_launches += vgraph_launches[prec];
     return cuda(cudaGraphLaunch(vgraph[prec], stream), "graph launch");
+  }
+  // fp32 V-cycle on the finest level (input vb, output vx1) with r.z of the mixed PCG
+  // fused into its last colour pass where the kernel supports it (rz_nparts > 0)
+  ipmg_status vcycle_rz(int L) {
+    static const bool fuse = [] {   // IPMG_RZ_FUSE=0: separate dot kernel (A/B runs)
+      const char* e = std::getenv("IPMG_RZ_FUSE");
+      return !(e && e[0] == '0');
+    }();
+    rz_r = fuse ? r : nullptr;
+    rz_part = partial;
+    rz_nparts = 0;
+    const ipmg_status st = vcycle_level(L, IPMG_FP32);
+    rz_r = nullptr;
+    rz_part = nullptr;
+    return st;
   }
   ipmg_status vcycle(const double* r, double* z, double* rz_partial) {
     const int prec = cfg.vcycle_precision;
@@ -1035,11 +1066,10 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
     if (mixed) {
       h->n_launches += 1;
       CK(ipmg::cast(0, 1, h->r, r32, n, s), "cast");
-      st = h->vcycle_level(L, IPMG_FP32);
-      if (st != IPMG_OK) return st;
-      h->n_launches += 3;
-      TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
-      CK(ipmg::finalize(h->partial, h->scal + cur, s), "finalize");
+      if ((st = h->vcycle_rz(L)) != IPMG_OK) return st;
+      h->n_launches += h->rz_nparts > 0 ? 2 : 3;
+      if (h->rz_nparts == 0) TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
+      CK(ipmg::finalize(h->partial, h->scal + cur, s, h->rz_nparts > 0 ? h->rz_nparts : -1), "finalize");
       if ((st = h->allsum(h->scal + cur)) != IPMG_OK) return st;
       TK(ipmg::cg_update_p32(h->p, z32, n, h->scal, cur, -1, s), 12.0 * n, "p = z");
     } else {
@@ -1082,11 +1112,10 @@ ipmg_status ipmg_cg_solve(ipmg_handle* h, const double* b, double* x, double rto
         break;
       }
       if (mixed) {
-        st = h->vcycle_level(L, IPMG_FP32);
-        if (st != IPMG_OK) return st;
-        h->n_launches += 3;
-        TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
-        CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s), "finalize");
+        if ((st = h->vcycle_rz(L)) != IPMG_OK) return st;
+        h->n_launches += h->rz_nparts > 0 ? 2 : 3;
+        if (h->rz_nparts == 0) TK(ipmg::dot_partial(0, 1, h->r, z32, n, h->partial, s), 12.0 * n, "dot");
+        CK(ipmg::finalize(h->partial, h->scal + (1 - cur), s, h->rz_nparts > 0 ? h->rz_nparts : -1), "finalize");
         if ((st = h->allsum(h->scal + (1 - cur))) != IPMG_OK) return st;
         TK(ipmg::cg_update_xp32(x, h->p, z32, n, h->scal, 1 - cur, cur, 2, s), 36.0 * n, "update x, p");
       } else {

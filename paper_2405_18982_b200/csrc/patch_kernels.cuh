@@ -2323,7 +2323,8 @@ inline pair3::Deltas pair3_deltas(const LevelGeom& g, int colour) {
   return d;
 }
 template <int NPAIR>
-cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s) {
+cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const LevelGeom& g, int colour, cudaStream_t s,
+                                const double* rdot = nullptr, double* dotp = nullptr, long long* nparts = nullptr) {
   using C = pair3::PC<NPAIR>;
   LevelGeom gg = g;
   const int m0 = g.n[0] / 2 - (colour & 1);
@@ -2338,9 +2339,10 @@ cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const L
   if (e != cudaSuccess) return e;
   constexpr int TY = pair3::TY;
   const dim3 grid((unsigned)(gx + (colour != 0 && g.zsel != 2 ? 1 : 0)), (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
+  if (nparts) *nparts = (long long)gx * gy * gg.znb;   // fused r.z partials (full lattice)
   // a zero-start pass (xi == nullptr) has no neighbour staging and no face arrays: X only
   pair3::smooth_pair3_kernel<NPAIR><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>((const float*)xi, (const float*)b, (float*)xo, gg,
-                                                               colour, gx, gy, pair3_deltas(g, colour));
+                                                               colour, gx, gy, pair3_deltas(g, colour), rdot, dotp);
   return cudaGetLastError();
 }
 #endif
@@ -2602,6 +2604,23 @@ inline cudaError_t vmult(int dim, int prec, const void* x, void* y, const LevelG
                          long long* nparts, cudaStream_t s) {
   return IPMG_DISPATCH(dim, prec, launch_vmult, x, y, g, bm, dotp, nparts, s);
 }
+// Colour pass with the r.z of the mixed PCG fused in (3D fp32 colour 0 through the pair
+// kernel: every dof is stored by exactly one patch): partials of sum r_i x_out_i into dotp,
+// *nparts = their count; any other case runs the plain pass and sets *nparts = 0.
+inline cudaError_t smooth_rz(int dim, int prec, const void* xi, const void* b, void* xo, const LevelGeom& g, int c,
+                             const double* r, double* dotp, long long* nparts, cudaStream_t s) {
+  *nparts = 0;
+#if !IPMG_DIRICHLET
+  if (dim == 3 && prec == 1 && c == 0 && xi != nullptr && pair3_enabled() && g.grouped && g.n[0] >= 2 &&
+      g.n[1] >= 2 && g.n[2] >= 2 && (reinterpret_cast<unsigned long long>(xi) & 15) == 0 && (g.ncells % 4) == 0 &&
+      (reinterpret_cast<unsigned long long>(xo) & 3) == 0) {
+    const cudaError_t e = launch_smooth_pair3<IPMG_PAIR3_NPAIR>(xi, b, xo, g, c, s, r, dotp, nparts);
+    if (e != cudaErrorNotReady) return e;
+    *nparts = 0;
+  }
+#endif
+  return IPMG_DISPATCH(dim, prec, launch_smooth, xi, b, xo, g, c, s);
+}
 inline cudaError_t smooth(int dim, int prec, const void* xi, const void* b, void* xo, const LevelGeom& g, int c,
                           cudaStream_t s) {
   return IPMG_DISPATCH(dim, prec, launch_smooth, xi, b, xo, g, c, s);
@@ -2639,6 +2658,7 @@ extern "C++" ipmg::KernelSet IPMG_CAT(ipmg_kernel_set_k, IPMG_K)() {
   ks.upload = ipmg::IPMG_KK::upload;
   ks.vmult = ipmg::IPMG_KK::vmult;
   ks.smooth = ipmg::IPMG_KK::smooth;
+  ks.smooth_rz = ipmg::IPMG_KK::smooth_rz;
   ks.additive = ipmg::IPMG_KK::additive;
   ks.restrict_ = ipmg::IPMG_KK::restrict_;
   ks.prolong = ipmg::IPMG_KK::prolong;

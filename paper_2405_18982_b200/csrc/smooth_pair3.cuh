@@ -227,22 +227,34 @@ __device__ __forceinline__ void load_b_rows(const float* __restrict__ b, const P
   for (int j = 0; j < NP; ++j) v[j] = scale == 1.f ? make_float2(lo[0][j], lo[1][j]) : mul2(make_float2(lo[0][j], lo[1][j]), f2(scale));
 }
 
+// stores the x-line pair's rows; rdot != nullptr: returns sum rdot[o] * (stored value) over
+// them (the r.z of the mixed PCG fused into the V-cycle's last colour pass, fp64)
 template <int NPAT>
-__device__ __forceinline__ void store_x_rows(float* __restrict__ x, const Pat<NPAT>& P, const Deltas& dl, int q, int i1,
-                                             int i2, const float2 (&v)[NP]) {
+__device__ __forceinline__ double store_x_rows(float* __restrict__ x, const Pat<NPAT>& P, const Deltas& dl, int q,
+                                               int i1, int i2, const float2 (&v)[NP],
+                                               const double* __restrict__ rdot) {
   const int qlo = 2 * (i1 / NC) + 4 * (i2 / NC), r0 = NC * (i1 % NC) + NC * NC * (i2 % NC);
+  double dot = 0.0;
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int p = 2 * q + s;
     if (!P.valid[p] || !((P.own[p] >> (i2 / NC)) & 1)) continue;   // ghost cells of a straddling patch
-    float* d0 = x + (long long)(P.base[p] + dl.pc[qlo]) * CELL + r0;
-    float* d1 = x + (long long)(P.base[p] + dl.pc[qlo + 1]) * CELL + r0;
+    const long long o0 = (long long)(P.base[p] + dl.pc[qlo]) * CELL + r0;
+    const long long o1 = (long long)(P.base[p] + dl.pc[qlo + 1]) * CELL + r0;
+    float* d0 = x + o0;
+    float* d1 = x + o1;
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
-      d0[j] = s ? v[j].y : v[j].x;
-      d1[j] = s ? v[NC + j].y : v[NC + j].x;
+      const float a0 = s ? v[j].y : v[j].x, a1 = s ? v[NC + j].y : v[NC + j].x;
+      d0[j] = a0;
+      d1[j] = a1;
+      if (rdot != nullptr) {
+        dot = fma(__ldg(rdot + o0 + j), (double)a0, dot);
+        dot = fma(__ldg(rdot + o1 + j), (double)a1, dot);
+      }
     }
   }
+  return dot;
 }
 
 // Trace unit (pair q, family a, side s, tangential cell h, second tangential index ic):
@@ -315,11 +327,11 @@ __device__ __forceinline__ void trace_unit(float2* F, const float* NBs, const fl
 // the pair kernel; FAST: every valid patch of the CTA is interior (variant 0 in all
 // directions) -> even/odd factors with compile-time constants
 template <int NPAIR, bool FAST>
-__device__ __forceinline__ void pair_body(const float* __restrict__ x_in, const float* __restrict__ b,
-                                          float* __restrict__ x_out, const LevelGeom& g, const Pat<2 * NPAIR>& P,
-                                          const Deltas& dl, float2* X, float2* F, const float* NBs,
-                                          const float* zslot, const float2 (&brow)[NP], int ybase, int zbase, int zq,
-                                          int zm0, int zm1) {
+__device__ __forceinline__ double pair_body(const float* __restrict__ x_in, const float* __restrict__ b,
+                                            float* __restrict__ x_out, const LevelGeom& g, const Pat<2 * NPAIR>& P,
+                                            const Deltas& dl, float2* X, float2* F, const float* NBs,
+                                            const float* zslot, const float2 (&brow)[NP], int ybase, int zbase,
+                                            int zq, int zm0, int zm1, const double* __restrict__ rdot) {
   using C = PC<NPAIR>;
   const TabData<K, float>& tb = c_tab32;
   const int t = threadIdx.x;
@@ -468,8 +480,9 @@ __device__ __forceinline__ void pair_body(const float* __restrict__ x_in, const 
     float2 v[NP], w[NP];
     ld_line(X, q0 * TSZ + S1 * i1 + S2 * i2, 1, v);
     bwd<FAST>(v, w, vx0, vx1);
-    store_x_rows(x_out, P, dl, q0, i1, i2, w);
+    return store_x_rows(x_out, P, dl, q0, i1, i2, w, rdot);
   }
+  return 0.0;
 }
 
 #ifndef IPMG_PAIR3_MINB
@@ -483,7 +496,8 @@ template <int NPAIR>
 __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
     smooth_pair3_kernel(const float* __restrict__ x_in, const float* __restrict__ b, float* __restrict__ x_out,
                         LevelGeom g, int colour, int gx, int gy,
-                        const __grid_constant__ Deltas dl) {
+                        const __grid_constant__ Deltas dl, const double* __restrict__ rdot,
+                        double* __restrict__ dot_partial) {
   using C = PC<NPAIR>;
   constexpr int NPAT = C::NPAT;
   // Grid (gx + 1, TY * gz, ceil(gy / TY)) over the colour's pair lattice (gx pairs per
@@ -680,10 +694,23 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
 #else
     if (P.valid[p] && (P.var[p][0] | P.var[p][1] | P.var[p][2])) allint = false;
 #endif
-  if (allint)
-    pair_body<NPAIR, true>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0, zm1);
-  else
-    pair_body<NPAIR, false>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0, zm1);
+  double d = allint ? pair_body<NPAIR, true>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0,
+                                             zm1, rdot)
+                    : pair_body<NPAIR, false>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq,
+                                              zm0, zm1, rdot);
+  if (dot_partial != nullptr) {
+    // fused r.z (colour 0 only: every dof is stored by exactly one patch): deterministic
+    // CTA partial (fixed tree), index over the full (x, y, z) patch-pair lattice
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    __shared__ double wsum[C::NT / 32];
+    if ((t & 31) == 0) wsum[t >> 5] = d;
+    __syncthreads();
+    if (t == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < C::NT / 32; ++w) sum += wsum[w];
+      dot_partial[bxi + (long long)gx * (byi + (long long)gy * bzi)] = sum;
+    }
+  }
 }
 
 }  // namespace pair3
