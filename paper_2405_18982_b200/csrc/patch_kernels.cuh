@@ -2335,14 +2335,19 @@ cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const L
   m2 = slab_sel_count(m2, g.zsel);
   const int gx = (m0 + C::NPAT - 1) / C::NPAT, gy = m1 > 0 ? m1 : 0, gz = m2;
   if ((long long)gx * gy * gz == 0) return cudaErrorNotReady;   // empty patch lattice: the caller copies
-  cudaError_t e = set_smem(pair3::smooth_pair3_kernel<NPAIR>, C::SMEM);
+  cudaError_t e = dotp ? set_smem(pair3::smooth_pair3_kernel<NPAIR, true>, C::SMEM)
+                       : set_smem(pair3::smooth_pair3_kernel<NPAIR, false>, C::SMEM);
   if (e != cudaSuccess) return e;
   constexpr int TY = pair3::TY;
   const dim3 grid((unsigned)(gx + (colour != 0 && g.zsel != 2 ? 1 : 0)), (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
   if (nparts) *nparts = (long long)gx * gy * gg.znb;   // fused r.z partials (full lattice)
   // a zero-start pass (xi == nullptr) has no neighbour staging and no face arrays: X only
-  pair3::smooth_pair3_kernel<NPAIR><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>((const float*)xi, (const float*)b, (float*)xo, gg,
-                                                               colour, gx, gy, pair3_deltas(g, colour), rdot, dotp);
+  if (dotp)
+    pair3::smooth_pair3_kernel<NPAIR, true><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>(
+        (const float*)xi, (const float*)b, (float*)xo, gg, colour, gx, gy, pair3_deltas(g, colour), rdot, dotp);
+  else
+    pair3::smooth_pair3_kernel<NPAIR, false><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>(
+        (const float*)xi, (const float*)b, (float*)xo, gg, colour, gx, gy, pair3_deltas(g, colour), nullptr, nullptr);
   return cudaGetLastError();
 }
 #endif

@@ -229,7 +229,7 @@ __device__ __forceinline__ void load_b_rows(const float* __restrict__ b, const P
 
 // stores the x-line pair's rows; rdot != nullptr: returns sum rdot[o] * (stored value) over
 // them (the r.z of the mixed PCG fused into the V-cycle's last colour pass, fp64)
-template <int NPAT>
+template <bool DOT, int NPAT>
 __device__ __forceinline__ double store_x_rows(float* __restrict__ x, const Pat<NPAT>& P, const Deltas& dl, int q,
                                                int i1, int i2, const float2 (&v)[NP],
                                                const double* __restrict__ rdot) {
@@ -248,7 +248,7 @@ __device__ __forceinline__ double store_x_rows(float* __restrict__ x, const Pat<
       const float a0 = s ? v[j].y : v[j].x, a1 = s ? v[NC + j].y : v[NC + j].x;
       d0[j] = a0;
       d1[j] = a1;
-      if (rdot != nullptr) {
+      if (DOT) {
         dot = fma(__ldg(rdot + o0 + j), (double)a0, dot);
         dot = fma(__ldg(rdot + o1 + j), (double)a1, dot);
       }
@@ -326,7 +326,7 @@ __device__ __forceinline__ void trace_unit(float2* F, const float* NBs, const fl
 
 // the pair kernel; FAST: every valid patch of the CTA is interior (variant 0 in all
 // directions) -> even/odd factors with compile-time constants
-template <int NPAIR, bool FAST>
+template <int NPAIR, bool FAST, bool DOT>
 __device__ __forceinline__ double pair_body(const float* __restrict__ x_in, const float* __restrict__ b,
                                             float* __restrict__ x_out, const LevelGeom& g, const Pat<2 * NPAIR>& P,
                                             const Deltas& dl, float2* X, float2* F, const float* NBs,
@@ -480,7 +480,7 @@ __device__ __forceinline__ double pair_body(const float* __restrict__ x_in, cons
     float2 v[NP], w[NP];
     ld_line(X, q0 * TSZ + S1 * i1 + S2 * i2, 1, v);
     bwd<FAST>(v, w, vx0, vx1);
-    return store_x_rows(x_out, P, dl, q0, i1, i2, w, rdot);
+    return store_x_rows<DOT>(x_out, P, dl, q0, i1, i2, w, rdot);
   }
   return 0.0;
 }
@@ -492,8 +492,10 @@ __device__ __forceinline__ double pair_body(const float* __restrict__ x_in, cons
 #define IPMG_PAIR3_TY 8   // rows per traversal tile (see the kernel); C4 DRAM reads 12.74 -> 8.96 GB
 #endif
 constexpr int TY = IPMG_PAIR3_TY;
-template <int NPAIR>
-__global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
+// DOT: the fused r.z variant (its own instantiation: the extra live values would cost the
+// plain passes registers -- 96 instead of 78 when it was one kernel)
+template <int NPAIR, bool DOT>
+__global__ void __launch_bounds__(PC<NPAIR>::NT, DOT ? 6 : IPMG_PAIR3_MINB)
     smooth_pair3_kernel(const float* __restrict__ x_in, const float* __restrict__ b, float* __restrict__ x_out,
                         LevelGeom g, int colour, int gx, int gy,
                         const __grid_constant__ Deltas dl, const double* __restrict__ rdot,
@@ -694,11 +696,11 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, IPMG_PAIR3_MINB)
 #else
     if (P.valid[p] && (P.var[p][0] | P.var[p][1] | P.var[p][2])) allint = false;
 #endif
-  double d = allint ? pair_body<NPAIR, true>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0,
+  double d = allint ? pair_body<NPAIR, true, DOT>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0,
                                              zm1, rdot)
-                    : pair_body<NPAIR, false>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq,
+                    : pair_body<NPAIR, false, DOT>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq,
                                               zm0, zm1, rdot);
-  if (dot_partial != nullptr) {
+  if (DOT) {
     // fused r.z (colour 0 only: every dof is stored by exactly one patch): deterministic
     // CTA partial (fixed tree), index over the full (x, y, z) patch-pair lattice
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
