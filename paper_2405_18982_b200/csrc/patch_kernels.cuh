@@ -2335,18 +2335,22 @@ cudaError_t launch_smooth_pair3(const void* xi, const void* b, void* xo, const L
   m2 = slab_sel_count(m2, g.zsel);
   const int gx = (m0 + C::NPAT - 1) / C::NPAT, gy = m1 > 0 ? m1 : 0, gz = m2;
   if ((long long)gx * gy * gz == 0) return cudaErrorNotReady;   // empty patch lattice: the caller copies
-  cudaError_t e = dotp ? set_smem(pair3::smooth_pair3_kernel<NPAIR, true>, C::SMEM)
-                       : set_smem(pair3::smooth_pair3_kernel<NPAIR, false>, C::SMEM);
+  cudaError_t e = dotp ? set_smem(pair3::smooth_pair3_kernel<NPAIR, true, true>, C::SMEM)
+                       : (xi ? set_smem(pair3::smooth_pair3_kernel<NPAIR, false, true>, C::SMEM)
+                             : set_smem(pair3::smooth_pair3_kernel<NPAIR, false, false>, C::XB));
   if (e != cudaSuccess) return e;
   constexpr int TY = pair3::TY;
   const dim3 grid((unsigned)(gx + (colour != 0 && g.zsel != 2 ? 1 : 0)), (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
   if (nparts) *nparts = (long long)gx * gy * gg.znb;   // fused r.z partials (full lattice)
   // a zero-start pass (xi == nullptr) has no neighbour staging and no face arrays: X only
   if (dotp)
-    pair3::smooth_pair3_kernel<NPAIR, true><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>(
+    pair3::smooth_pair3_kernel<NPAIR, true, true><<<grid, C::NT, C::SMEM, s>>>(
         (const float*)xi, (const float*)b, (float*)xo, gg, colour, gx, gy, pair3_deltas(g, colour), rdot, dotp);
+  else if (xi)
+    pair3::smooth_pair3_kernel<NPAIR, false, true><<<grid, C::NT, C::SMEM, s>>>(
+        (const float*)xi, (const float*)b, (float*)xo, gg, colour, gx, gy, pair3_deltas(g, colour), nullptr, nullptr);
   else
-    pair3::smooth_pair3_kernel<NPAIR, false><<<grid, C::NT, xi ? C::SMEM : C::XB, s>>>(
+    pair3::smooth_pair3_kernel<NPAIR, false, false><<<grid, C::NT, C::XB, s>>>(
         (const float*)xi, (const float*)b, (float*)xo, gg, colour, gx, gy, pair3_deltas(g, colour), nullptr, nullptr);
   return cudaGetLastError();
 }
@@ -2358,13 +2362,12 @@ cudaError_t launch_smooth(const void* xi, const void* b, void* xo, const LevelGe
 #if !IPMG_DIRICHLET
   // the pair kernel's TMA copies need a 16-byte aligned x_in whose cell range ends on a
   // 16-byte boundary (the copies are widened to 16-byte granularity)
-  // (zero-start passes, x_in == nullptr, stay on smooth_kernel: without face traces the
-  // pair kernel's fewer instructions do not make up for its lower occupancy, measured
-  // 3D k=4 colour 0 from zero 0.84 vs 0.94 ms)
 #ifndef IPMG_PAIR3_ZERO
-#define IPMG_PAIR3_ZERO 0   // 1: zero-start passes (x_in == nullptr) through the pair kernel too
+#define IPMG_PAIR3_ZERO 0x10   // degrees whose zero-start passes (x_in == nullptr) also take the pair
+                               // kernel (its FACES = false instantiation, 56 registers, X-only shared
+                               // memory): 3D k=4 colour 0 from zero 0.839 -> 0.774 ms
 #endif
-  if (D == 3 && sizeof(T) == 4 && (xi != nullptr || IPMG_PAIR3_ZERO) && pair3_enabled() && g.grouped &&
+  if (D == 3 && sizeof(T) == 4 && (xi != nullptr || ((IPMG_PAIR3_ZERO >> K) & 1)) && pair3_enabled() && g.grouped &&
       g.n[0] >= 2 && g.n[1] >= 2 && g.n[2] >= 2 &&
       (reinterpret_cast<unsigned long long>(xi) & 15) == 0 && (g.ncells % 4) == 0 &&
       (reinterpret_cast<unsigned long long>(xo) & 3) == 0) {

@@ -326,7 +326,7 @@ __device__ __forceinline__ void trace_unit(float2* F, const float* NBs, const fl
 
 // the pair kernel; FAST: every valid patch of the CTA is interior (variant 0 in all
 // directions) -> even/odd factors with compile-time constants
-template <int NPAIR, bool FAST, bool DOT>
+template <int NPAIR, bool FAST, bool DOT, bool FACES>
 __device__ __forceinline__ double pair_body(const float* __restrict__ x_in, const float* __restrict__ b,
                                             float* __restrict__ x_out, const LevelGeom& g, const Pat<2 * NPAIR>& P,
                                             const Deltas& dl, float2* X, float2* F, const float* NBs,
@@ -335,7 +335,7 @@ __device__ __forceinline__ double pair_body(const float* __restrict__ x_in, cons
   using C = PC<NPAIR>;
   const TabData<K, float>& tb = c_tab32;
   const int t = threadIdx.x;
-  const bool faces = x_in != nullptr;
+  const bool faces = FACES && x_in != nullptr;
   if (faces) {
     cp_async_wait_all();
     __syncthreads();
@@ -494,7 +494,9 @@ __device__ __forceinline__ double pair_body(const float* __restrict__ x_in, cons
 constexpr int TY = IPMG_PAIR3_TY;
 // DOT: the fused r.z variant (its own instantiation: the extra live values would cost the
 // plain passes registers -- 96 instead of 78 when it was one kernel)
-template <int NPAIR, bool DOT>
+// FACES = false: the zero-start pass (x_in == nullptr) as its own instantiation without the
+// staging and trace code (fewer registers, X-only shared memory)
+template <int NPAIR, bool DOT, bool FACES>
 __global__ void __launch_bounds__(PC<NPAIR>::NT, DOT ? 6 : IPMG_PAIR3_MINB)
     smooth_pair3_kernel(const float* __restrict__ x_in, const float* __restrict__ b, float* __restrict__ x_out,
                         LevelGeom g, int colour, int gx, int gy,
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, DOT ? 6 : IPMG_PAIR3_MINB)
     }
   }
 #endif
-  if (x_in != nullptr) {
+  if (FACES && x_in != nullptr) {
     // face-neighbour cells -> shared memory: 16-byte cp.async, a warp per cell (lanes on
     // consecutive chunks), each copy widened to the 16-byte boundaries around the cell
     // (inside the vector: its base and end are 16-byte aligned, checked by the launcher).
@@ -651,7 +653,7 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, DOT ? 6 : IPMG_PAIR3_MINB)
   // the first one at or above its end: inside the vector whenever its base and end are
   // 16-byte aligned (checked by the launcher).  First the source of every cell (one
   // thread per cell), then the copies.
-  if (x_in != nullptr) {
+  if (FACES && x_in != nullptr) {
     // entry: the 16-byte aligned source address, its low bits the cell's float offset
     // from that boundary (0..3)
     for (int e = t; e < NPAT * NNB; e += C::NT) {
@@ -696,9 +698,9 @@ __global__ void __launch_bounds__(PC<NPAIR>::NT, DOT ? 6 : IPMG_PAIR3_MINB)
 #else
     if (P.valid[p] && (P.var[p][0] | P.var[p][1] | P.var[p][2])) allint = false;
 #endif
-  double d = allint ? pair_body<NPAIR, true, DOT>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0,
+  double d = allint ? pair_body<NPAIR, true, DOT, FACES>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq, zm0,
                                              zm1, rdot)
-                    : pair_body<NPAIR, false, DOT>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq,
+                    : pair_body<NPAIR, false, DOT, FACES>(x_in, b, x_out, g, P, dl, X, F, NBs, zslot, brow, ybase, zbase, zq,
                                               zm0, zm1, rdot);
   if (DOT) {
     // fused r.z (colour 0 only: every dof is stored by exactly one patch): deterministic
