@@ -3,8 +3,9 @@
 //
 // One CTA processes PPC vertex patches of one colour.  Each patch is staged in
 // shared memory as a patch-lexicographic tensor of (2(k+1))^d values (odd row
-// pitch; plane and patch pitches padded by a compile-time search so that the
-// line passes are shared-memory bank-conflict free), loaded and stored with
+// pitch; plane and patch pitches padded by a compile-time search that minimises the
+// bank conflicts of the line passes -- the face-trace loads and stores still conflict,
+// ncu counts in profiles/), loaded and stored with
 // coalesced (vectorised where the cell size allows) cooperative copies of
 // whole cell chunks.  Every sum-factorisation step is a "line pass": a thread
 // owns R whole 1D lines of one patch along one direction (R = 2 in fp32, 1 in

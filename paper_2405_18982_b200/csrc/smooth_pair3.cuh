@@ -17,6 +17,9 @@
 //    NP(NP+1)): x-lines (i1 fastest) are bank-conflict free; y- and z-lines are
 //    dealt to threads by host-built tables that put 16 distinct banks into every
 //    half warp (conflict free whenever no residue class exceeds the half-warp count).
+//    The trace units' loads from the staged cells are not conflict free: the per-cell
+//    alignment offsets and the slot pitch put lanes of different cells on the same bank
+//    (ncu at C4: ~270 M excess shared load wavefronts per pass, profiles/r02j_ncu_full.md).
 //  * the face-neighbour cells are copied into shared memory with 16-byte cp.async
 //    (a warp per cell, lanes on consecutive 16-byte chunks: one instruction per cell
 //    and fully used lines; TMA bulk copies measured slower -- every copy needs its own
