@@ -459,8 +459,8 @@ def run_ours(args, rank, ws, local):
     else:
         roof = {"bound": "alu", "achieved": tf_eo, "peak": alu_fp32, "unit": "TFLOP/s",
                 "frac": tf_eo / alu_fp32, "traffic": traffic}
-    kname = ("smooth_pair3_kernel (patch pairs, k=%d) for colour passes with x, smooth_kernel<3,float> from zero"
-             % wl["degree"]) if (wl["dim"] == 3 and wl["degree"] == 4) else "smooth_kernel<%d,float> (k=%d)" % (
+    kname = ("smooth_pair3_kernel (patch pairs, k=%d): colour passes with x, the zero-start instantiation "
+             "(colour 0 from x = 0) and the fused-r.z instantiation (last post-smoothing colour)" % wl["degree"]) if (wl["dim"] == 3 and wl["degree"] == 4) else "smooth_kernel<%d,float> (k=%d)" % (
                  wl["dim"], wl["degree"])
     roof.update({"kernel": kname + ", finest level colour passes",
                  "peak_source": {"hbm": src, "alu": "measured live (ipmg_alu_peak FFMA2)"},
