@@ -41,61 +41,64 @@ constexpr int FROW = NP;                                    // face array: t1 fa
 constexpr int FARR = NP * FROW + 1;                         // array pitch (odd)
 constexpr int NNB = 24;
 // a staged cell: the copy covers the cell from the 16-byte boundary at or below its start
-// to the one at or above its end; 8-byte cell starts make that ceil((8 CELL + 8) / 16)
-// chunks at most
-constexpr int CHUNKS = (8 * CELL + 8 + 15) / 16;
-constexpr int SLOT = 2 * CHUNKS;                            // doubles per slot
+// to the one at or above its end: ceil((CELL sizeof(T) + 16 - sizeof(T)) / 16) chunks at most
+template <typename T>
+struct Lay {
+  static constexpr int EPC = 16 / (int)sizeof(T);                                // elements per chunk
+  static constexpr int CHUNKS = ((int)sizeof(T) * CELL + 16 - (int)sizeof(T) + 15) / 16;
+  static constexpr int SLOT = EPC * CHUNKS;                                       // elements per slot
+  static constexpr size_t NBB = sizeof(T) * (size_t)NNB * SLOT;
+  static constexpr size_t XB = sizeof(T) * 2 * (size_t)TSZ;                      // X and T1 (alias the slots)
+  static constexpr size_t OWNB = IPMG_OP3_STAGE_OWN ? sizeof(T) * 8 * (size_t)SLOT : 0;
+  static constexpr size_t FB = sizeof(T) * 12 * (size_t)FARR;
+  static constexpr size_t SMEM = NBB + OWNB + FB;
+  static_assert(XB <= NBB, "op3: X, T1 alias the neighbour slots");
+};
 constexpr int NT = (((NL > 12 * NP ? NL : 12 * NP) + 31) / 32) * 32;   // a line / trace unit per thread
 static_assert(NT <= pair3::NTMAX, "line tables");
 constexpr int NSTAGE = NNB + (IPMG_OP3_STAGE_OWN ? 8 : 0);  // staged cells
-constexpr size_t NBB = sizeof(double) * (size_t)NNB * SLOT;
-constexpr size_t XB = sizeof(double) * 2 * (size_t)TSZ;     // X and T1 (alias the neighbour slots)
-constexpr size_t OWNB = IPMG_OP3_STAGE_OWN ? sizeof(double) * 8 * (size_t)SLOT : 0;
-constexpr size_t FB = sizeof(double) * 12 * (size_t)FARR;
-constexpr size_t SMEM = NBB + OWNB + FB;
-static_assert(XB <= NBB, "op3: X, T1 alias the neighbour slots");
 
 __device__ __forceinline__ int farr(int a, int s, int kind) { return ((a * 2 + s) * 2 + kind) * FARR; }
-// doubles between a staged cell's slot start and the cell: 1 when the cell starts 8 bytes
-// past a 16-byte boundary (odd cell index and odd CELL; x is 16-byte aligned)
-__device__ __forceinline__ int soff(long long cell) { return (int)(cell & (long long)(CELL & 1)); }
+// elements between a staged cell's slot start and the cell (x is 16-byte aligned)
+template <typename T>
+__device__ __forceinline__ int soff(long long cell) { return (int)((cell * CELL) & (long long)(Lay<T>::EPC - 1)); }
 
 // Trace unit of family A (compile-time: one code path per family, no selects):
 // u[lb] = x(face node), du[lb] = sum_j phi_j'(face) x_j of the neighbour across face
 // (A, s) at the NC face points lb along t1 in t1-cell h, second tangential index ic;
 // families 1 and 2 get the cell mass along t1 (= x) applied.
-template <int A>
-__device__ __forceinline__ void trace_unit(double* F, const double* c, bool exists, int s, int h, int ic) {
-  const TabData<K, double>& tb = tab<double>();
+template <int A, typename T>
+__device__ __forceinline__ void trace_unit(T* F, const T* c, bool exists, int s, int h, int ic) {
+  const TabData<K, T>& tb = tab<T>();
   const int lc = ic % NC;
-  double u[NC], du[NC];
+  T u[NC], du[NC];
   if (exists) {
     const int jf = s == 0 ? NC - 1 : 0;   // face node: the neighbour's last node (low side), first (high)
     // element (normal j, point lb) of the 5x5 block at c + PS * lb + NS * j + TS * lc
     constexpr int PS = A == 0 ? NC : 1;            // point stride (t1 = y for A = 0, x otherwise)
     constexpr int NS = A == 0 ? 1 : (A == 1 ? NC : NC * NC);
     constexpr int TS = A == 2 ? NC : NC * NC;      // second tangential (t2 = z, z, y)
-    const double* b0 = c + TS * lc;
-    double v[NC][NC];   // [point][normal]
+    const T* b0 = c + TS * lc;
+    T v[NC][NC];   // [point][normal]
 #pragma unroll
     for (int lb = 0; lb < NC; ++lb)
 #pragma unroll
       for (int j = 0; j < NC; ++j) v[lb][j] = b0[PS * lb + NS * j];
 #pragma unroll
     for (int lb = 0; lb < NC; ++lb) {
-      double acc = 0.0;
+      T acc = T(0);
 #pragma unroll
-      for (int j = 0; j < NC; ++j) acc = fma(s == 0 ? tb.d1[j] : tb.d0[j], v[lb][j], acc);
+      for (int j = 0; j < NC; ++j) acc = fma_(s == 0 ? tb.d1[j] : tb.d0[j], v[lb][j], acc);
       du[lb] = acc;
       u[lb] = s == 0 ? v[lb][NC - 1] : v[lb][0];
     }
     (void)jf;
   } else {
 #pragma unroll
-    for (int lb = 0; lb < NC; ++lb) u[lb] = du[lb] = 0.0;
+    for (int lb = 0; lb < NC; ++lb) u[lb] = du[lb] = T(0);
   }
-  double* fu = F + farr(A, s, 0) + h * NC + FROW * ic;
-  double* fd = F + farr(A, s, 1) + h * NC + FROW * ic;
+  T* fu = F + farr(A, s, 0) + h * NC + FROW * ic;
+  T* fd = F + farr(A, s, 1) + h * NC + FROW * ic;
   if (A == 0) {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -105,11 +108,11 @@ __device__ __forceinline__ void trace_unit(double* F, const double* c, bool exis
   } else {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
-      double mu = 0.0, md = 0.0;
+      T mu = T(0), md = T(0);
 #pragma unroll
       for (int lb = 0; lb < NC; ++lb) {
-        mu = fma(tb.M[lb][i], u[lb], mu);
-        md = fma(tb.M[lb][i], du[lb], md);
+        mu = fma_(tb.M[lb][i], u[lb], mu);
+        md = fma_(tb.M[lb][i], du[lb], md);
       }
       fu[i] = mu;
       fd[i] = md;
@@ -118,73 +121,77 @@ __device__ __forceinline__ void trace_unit(double* F, const double* c, bool exis
 }
 
 // second tangential mass (along y) of the z-normal family: line e of 40 = (side, kind, x index o)
-__device__ __forceinline__ void t2_mass(double* F, int e) {
+template <typename T>
+__device__ __forceinline__ void t2_mass(T* F, int e) {
   const int o = e % NP, sk = e / NP;   // sk = side * 2 + kind
-  double* base = F + farr(2, sk >> 1, sk & 1) + o;
-  double v[1][NP], w[1][NP];
+  T* base = F + farr(2, sk >> 1, sk & 1) + o;
+  T v[1][NP], w[1][NP];
   load_lines<NP, 1>(base, 0, FROW, v);
-  mv<NP, NP, MassP<double>, 1>(v, w);
+  mv<NP, NP, MassP<T>, 1>(v, w);
   store_lines<NP, 1>(base, 0, FROW, w);
 }
 
 // injection of face family a at tangential position pos into a line along a (operator sign +)
-__device__ __forceinline__ void inject(double (&y)[1][NP], const double* F, int a, int pos) {
-  const TabData<K, double>& tb = tab<double>();
-  const double ul = F[farr(a, 0, 0) + pos], dl = F[farr(a, 0, 1) + pos];
-  const double uh = F[farr(a, 1, 0) + pos], dh = F[farr(a, 1, 1) + pos];
+template <typename T>
+__device__ __forceinline__ void inject(T (&y)[1][NP], const T* F, int a, int pos) {
+  const TabData<K, T>& tb = tab<T>();
+  const T ul = F[farr(a, 0, 0) + pos], dl = F[farr(a, 0, 1) + pos];
+  const T uh = F[farr(a, 1, 0) + pos], dh = F[farr(a, 1, 1) + pos];
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
-    double lo = tb.CF[0][i] * ul;
-    if (i == 0) lo = fma(tb.CF[1][i], dl, lo);
+    T lo = tb.CF[0][i] * ul;
+    if (i == 0) lo = fma_(tb.CF[1][i], dl, lo);
     y[0][i] += lo;
-    double hi = tb.CF[2][NC + i] * uh;
-    if (i == NC - 1) hi = fma(tb.CF[3][NC + i], dh, hi);
+    T hi = tb.CF[2][NC + i] * uh;
+    if (i == NC - 1) hi = fma_(tb.CF[3][NC + i], dh, hi);
     y[0][NC + i] += hi;
   }
 }
 
-template <bool FAST>
-__device__ __forceinline__ void lap(const double (&v)[1][NP], double (&w)[1][NP], int var) {
-  if (FAST) mv<NP, NP, LapP<0, double>, 1>(v, w);
-  else if (var == 0) mv<NP, NP, LapP<0, double>, 1>(v, w);
-  else mv<NP, NP, LapRT<double>, 1>(v, w, LapRT<double>{var});
+template <bool FAST, typename T>
+__device__ __forceinline__ void lap(const T (&v)[1][NP], T (&w)[1][NP], int var) {
+  if (FAST) mv<NP, NP, LapP<0, T>, 1>(v, w);
+  else if (var == 0) mv<NP, NP, LapP<0, T>, 1>(v, w);
+  else mv<NP, NP, LapRT<T>, 1>(v, w, LapRT<T>{var});
 }
-template <bool FAST>
-__device__ __forceinline__ void lap_acc(const double (&v)[1][NP], double (&w)[1][NP], int var) {
-  if (FAST) mv_acc<NP, NP, LapP<0, double>, 1>(v, w);
-  else if (var == 0) mv_acc<NP, NP, LapP<0, double>, 1>(v, w);
-  else mv_acc<NP, NP, LapRT<double>, 1>(v, w, LapRT<double>{var});
+template <bool FAST, typename T>
+__device__ __forceinline__ void lap_acc(const T (&v)[1][NP], T (&w)[1][NP], int var) {
+  if (FAST) mv_acc<NP, NP, LapP<0, T>, 1>(v, w);
+  else if (var == 0) mv_acc<NP, NP, LapP<0, T>, 1>(v, w);
+  else mv_acc<NP, NP, LapRT<T>, 1>(v, w, LapRT<T>{var});
 }
 
 struct PatchInfo {
   int base, var[3], own;
 };
 
-template <bool FAST>
-__device__ __forceinline__ double op3_body(const double* __restrict__ x, double* __restrict__ y,
-                                           const double* __restrict__ bm, const LevelGeom& g, const PatchInfo& P,
-                                           const pair3::Deltas& dl, double* X, double* T1, const double* OWN,
-                                           double* F, bool dot) {
-  const TabData<K, double>& tb = tab<double>();
+// MODE 0: y = hs A x (or bm - hs A x) stored, fused x.y returned; MODE 1 (restriction):
+// r = b - hs A x formed on the z-lines and contracted with P^T along z in place (the
+// kernel then contracts y and x and writes the coarse cell)
+template <bool FAST, int MODE, typename T>
+__device__ __forceinline__ double op3_body(const T* __restrict__ x, T* __restrict__ y, const T* __restrict__ bm,
+                                           const LevelGeom& g, const PatchInfo& P, const pair3::Deltas& dl, T* X,
+                                           T* T1, const T* OWN, T* F, bool dot) {
+  using LY = Lay<T>;
   const int t = threadIdx.x;
   // ---- x pass: T1 = M0 x, X = L0 x + x-normal family; the z-normal family's y mass on idle threads
   if (t < NL) {
     const int i1 = t % NP, i2 = t / NP;
     const int qlo = 2 * (i1 / NC) + 4 * (i2 / NC), r0 = NC * (i1 % NC) + NC * NC * (i2 % NC);
-    double v[1][NP], w[1][NP];
+    T v[1][NP], w[1][NP];
 #if IPMG_OP3_STAGE_OWN
-    const double* s0 = OWN + qlo * SLOT + soff(P.base + dl.pc[qlo]) + r0;
-    const double* s1 = OWN + (qlo + 1) * SLOT + soff(P.base + dl.pc[qlo + 1]) + r0;
+    const T* s0 = OWN + qlo * LY::SLOT + soff<T>(P.base + dl.pc[qlo]) + r0;
+    const T* s1 = OWN + (qlo + 1) * LY::SLOT + soff<T>(P.base + dl.pc[qlo + 1]) + r0;
 #else
-    const double* s0 = x + (long long)(P.base + dl.pc[qlo]) * CELL + r0;
-    const double* s1 = x + (long long)(P.base + dl.pc[qlo + 1]) * CELL + r0;
+    const T* s0 = x + (long long)(P.base + dl.pc[qlo]) * CELL + r0;
+    const T* s1 = x + (long long)(P.base + dl.pc[qlo + 1]) * CELL + r0;
 #endif
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       v[0][j] = s0[j];
       v[0][NC + j] = s1[j];
     }
-    mv<NP, NP, MassP<double>, 1>(v, w);
+    mv<NP, NP, MassP<T>, 1>(v, w);
     store_lines<NP, 1>(T1 + S1 * i1 + S2 * i2, 0, 1, w);
     lap<FAST>(v, w, P.var[0]);
     inject(w, F, 0, i1 + FROW * i2);
@@ -199,47 +206,62 @@ __device__ __forceinline__ double op3_body(const double* __restrict__ x, double*
   const unsigned ly = __ldg(&pair3::g_lines[0][0][t]);
   if (ly != 0xffffffffu) {
     const int base = (int)ly, i0 = base % S2, i2 = base / S2;
-    double m[1][NP], lx[1][NP], w[1][NP];
+    T m[1][NP], lx[1][NP], w[1][NP];
     load_lines<NP, 1>(T1 + base, 0, S1, m);
     load_lines<NP, 1>(X + base, 0, S1, lx);
-    mv<NP, NP, MassP<double>, 1>(lx, w);
+    mv<NP, NP, MassP<T>, 1>(lx, w);
     lap_acc<FAST>(m, w, P.var[1]);
     inject(w, F, 1, i0 + FROW * i2);
     store_lines<NP, 1>(X + base, 0, S1, w);
-    mv<NP, NP, MassP<double>, 1>(m, w);
+    mv<NP, NP, MassP<T>, 1>(m, w);
     store_lines<NP, 1>(T1 + base, 0, S1, w);
   }
   __syncthreads();
-  // ---- z pass: y = hs (M2 X + L2 T1 + z-normal family) -> global (fused x.y)
+  // ---- z pass: hs (M2 X + L2 T1 + z-normal family)
   double dacc = 0.0;
   const unsigned lz = __ldg(&pair3::g_lines[0][1][t]);
   if (lz != 0xffffffffu) {
     const int base = (int)(lz & 0xffff), i0 = (lz >> 16) & 0xf, i1 = (lz >> 20) & 0xf;
-    double a[1][NP], bb[1][NP], w[1][NP];
+    T a[1][NP], bb[1][NP], w[1][NP];
     load_lines<NP, 1>(X + base, 0, S2, a);
-    mv<NP, NP, MassP<double>, 1>(a, w);
+    mv<NP, NP, MassP<T>, 1>(a, w);
     load_lines<NP, 1>(T1 + base, 0, S2, bb);
     lap_acc<FAST>(bb, w, P.var[2]);
     inject(w, F, 2, i0 + FROW * i1);
-    const double hs = g.hs;
+    const T hs = T(g.hs);
     const int qb = (i0 / NC) + 2 * (i1 / NC), ob = (i0 % NC) + NC * (i1 % NC);
+    if (MODE == 1) {
+      // residual on the z-line (b gathered along it), then P^T along z into the line's
+      // first NC entries (only this thread touches the line in this phase)
+      T r[1][NP], rc[1][NC];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      if (!((P.own >> c) & 1)) continue;   // ghost cells of a straddling patch
-      const long long cell = (long long)P.base + dl.pc[qb + 4 * c];
-      double* yo = y + cell * CELL + ob;
+      for (int c = 0; c < 2; ++c) {
+        const T* bo = bm + ((long long)P.base + dl.pc[qb + 4 * c]) * CELL + ob;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) r[0][c * NC + j] = fma_(-hs, w[0][c * NC + j], __ldg(bo + NC * NC * j));
+      }
+      mv<NC, NP, ProlT<T>, 1>(r, rc);
+#pragma unroll
+      for (int j = 0; j < NC; ++j) X[base + j * S2] = rc[0][j];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (!((P.own >> c) & 1)) continue;   // ghost cells of a straddling patch
+        const long long cell = (long long)P.base + dl.pc[qb + 4 * c];
+        T* yo = y + cell * CELL + ob;
 #if IPMG_OP3_STAGE_OWN
-      const double* xo = OWN + (qb + 4 * c) * SLOT + soff(cell) + ob;
+        const T* xo = OWN + (qb + 4 * c) * LY::SLOT + soff<T>(cell) + ob;
 #else
-      const double* xo = x + cell * CELL + ob;
+        const T* xo = x + cell * CELL + ob;
 #endif
-      const double* bo = bm ? bm + cell * CELL + ob : nullptr;
+        const T* bo = bm ? bm + cell * CELL + ob : nullptr;
 #pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        double val = hs * w[0][c * NC + j];
-        if (bo) val = __ldg(bo + NC * NC * j) - val;
-        yo[NC * NC * j] = val;
-        if (dot) dacc = fma(xo[NC * NC * j], val, dacc);
+        for (int j = 0; j < NC; ++j) {
+          T val = hs * w[0][c * NC + j];
+          if (bo) val = __ldg(bo + NC * NC * j) - val;
+          yo[NC * NC * j] = val;
+          if (dot) dacc = fma((double)xo[NC * NC * j], (double)val, dacc);
+        }
       }
     }
   }
@@ -251,25 +273,30 @@ __device__ __forceinline__ double op3_body(const double* __restrict__ x, double*
 #endif
 constexpr int TY = IPMG_OP3_TY;
 
-__global__ void __launch_bounds__(NT) op3_kernel(const double* __restrict__ x, double* __restrict__ y,
-                                                 const double* __restrict__ bm, LevelGeom g, int gx, int gy,
+// MODE 0: the operator (y = hs A x, or bm - hs A x; fused x.y partials when dot_partial).
+// MODE 1: the restriction r_c = P^T (bm - hs A x) of the patch (= parent cell) into rc on
+// the coarse level gc (restrict_kernel's contract).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(NT) op3_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                 const T* __restrict__ bm, LevelGeom g, int gx, int gy,
                                                  const __grid_constant__ pair3::Deltas dl,
-                                                 double* __restrict__ dot_partial) {
+                                                 double* __restrict__ dot_partial, LevelGeom gc) {
+  using LY = Lay<T>;
   // grid (gx, TY * gz, ceil(gy / TY)): tiles of TY patch rows, as the pair smoother
   const int bxi = blockIdx.x, byi = (int)blockIdx.z * TY + (int)(blockIdx.y % TY), jz = (int)(blockIdx.y / TY);
   if (byi >= gy) return;   // the last tile's missing rows (no partial: see the launcher)
   const int bzi = g.zsel == 0 ? jz : (g.zsel == 1 ? jz + 1 : (jz == 0 ? 0 : g.znb - 1));
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* NBs = reinterpret_cast<double*>(smem_raw);
-  double* X = NBs;   // X, T1 alias the neighbour slots (dead after the trace units)
-  double* T1 = NBs + TSZ;
-  double* OWN = NBs + NNB * SLOT;   // the own cells follow the neighbour slots (slot 24 + q)
-  double* F = reinterpret_cast<double*>(smem_raw + NBB + OWNB);
+  T* NBs = reinterpret_cast<T*>(smem_raw);
+  T* X = NBs;   // X, T1 alias the neighbour slots (dead after the trace units)
+  T* T1 = NBs + TSZ;
+  T* OWN = NBs + NNB * LY::SLOT;   // the own cells follow the neighbour slots (slot 24 + q)
+  T* F = reinterpret_cast<T*>(smem_raw + LY::NBB + LY::OWNB);
   const int t = threadIdx.x;
   // patch data in registers (every thread: no barrier, no shared table)
   PatchInfo P;
+  const int c0x = 2 * bxi, c0y = 2 * byi, c0z = 2 * bzi;   // colour 0: slab_first = 0
   {
-    const int c0x = 2 * bxi, c0y = 2 * byi, c0z = 2 * bzi;   // colour 0: slab_first = 0
     P.base = (int)cell_offset_cells(g, c0x, c0y, c0z);
     const int gs = g.zoff + c0z;
     P.own = (c0z >= 0 ? 1 : 0) | (c0z + 1 < g.n[2] ? 2 : 0);
@@ -305,12 +332,12 @@ __global__ void __launch_bounds__(NT) op3_kernel(const double* __restrict__ x, d
     for (int i = 0; i < PER; ++i) {
       if (w + NW * i >= NSTAGE) break;
       const unsigned long long src = __shfl_sync(0xffffffffu, my, i);
-      double* dst = NBs + (w + NW * i) * SLOT;
+      T* dst = NBs + (w + NW * i) * LY::SLOT;
       // chunks c0 + lane; lanes past the end repeat chunk CHUNKS - 1 (the same bytes): no branch
 #pragma unroll
-      for (int c0 = 0; c0 < CHUNKS; c0 += 32) {
-        const int c = c0 + lane < CHUNKS ? c0 + lane : CHUNKS - 1;
-        cp_async<16>(dst + 2 * c, reinterpret_cast<const void*>(src + 16ull * c));
+      for (int c0 = 0; c0 < LY::CHUNKS; c0 += 32) {
+        const int c = c0 + lane < LY::CHUNKS ? c0 + lane : LY::CHUNKS - 1;
+        cp_async<16>(dst + LY::EPC * c, reinterpret_cast<const void*>(src + 16ull * c));
       }
     }
     cp_async_commit();
@@ -325,16 +352,41 @@ __global__ void __launch_bounds__(NT) op3_kernel(const double* __restrict__ x, d
     const int k = (2 * a + s) * 4 + tc;
     const int va = a == 0 ? P.var[0] : (a == 1 ? P.var[1] : P.var[2]);
     const bool ex = !((va >> s) & 1);
-    const double* c = NBs + k * SLOT + (ex ? soff(P.base + dl.nb[k]) : 0);
+    const T* c = NBs + k * LY::SLOT + (ex ? soff<T>(P.base + dl.nb[k]) : 0);
     if (a == 0) trace_unit<0>(F, c, ex, s, h, ic);
     else if (a == 1) trace_unit<1>(F, c, ex, s, h, ic);
     else trace_unit<2>(F, c, ex, s, h, ic);
   }
   __syncthreads();
   const bool fast = (P.var[0] | P.var[1] | P.var[2]) == 0;
-  const bool dot = dot_partial != nullptr;
-  double d = fast ? op3_body<true>(x, y, bm, g, P, dl, X, T1, OWN, F, dot)
-                  : op3_body<false>(x, y, bm, g, P, dl, X, T1, OWN, F, dot);
+  const bool dot = MODE == 0 && dot_partial != nullptr;
+  double d = fast ? op3_body<true, MODE>(x, y, bm, g, P, dl, X, T1, (const T*)OWN, F, dot)
+                  : op3_body<false, MODE>(x, y, bm, g, P, dl, X, T1, (const T*)OWN, F, dot);
+  if (MODE == 1) {
+    // P^T along y on the lines (i0, i2 < NC) of the z-contracted slab, in place
+    __syncthreads();
+    if (t < NP * NC) {
+      const int i0 = t % NP, i2 = t / NP;
+      T v[1][NP], w[1][NC];
+      load_lines<NP, 1>(X + i0 + S2 * i2, 0, S1, v);
+      mv<NC, NP, ProlT<T>, 1>(v, w);
+#pragma unroll
+      for (int j = 0; j < NC; ++j) X[i0 + S2 * i2 + S1 * j] = w[0][j];
+    }
+    __syncthreads();
+    // P^T along x on the lines (i1, i2 < NC): one coarse-cell row each, straight to global
+    if (t < NC * NC) {
+      const int i1 = t % NC, i2 = t / NC;
+      T v[1][NP], w[1][NC];
+      load_lines<NP, 1>(X + S1 * i1 + S2 * i2, 0, 1, v);
+      mv<NC, NP, ProlT<T>, 1>(v, w);
+      const int c0[3] = {c0x, c0y, c0z};
+      T* dst = y + coarse_cell<3>(g, gc, c0) * CELL + NC * i1 + NC * NC * i2;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) dst[j] = w[0][j];
+    }
+    return;
+  }
   if (dot) {
     // fused x.y of CG: deterministic CTA partial (fixed tree), full-grid index
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);

@@ -2213,13 +2213,13 @@ inline cudaError_t launch_op3(const void* x, void* y, const LevelGeom& g, const 
   if (nparts) *nparts = (long long)gx * gy * gg.znb;   // full grid
   if (x == nullptr) return cudaSuccess;               // size query
   if ((reinterpret_cast<unsigned long long>(x) & 15) != 0 || (g.ncells % 2) != 0) return cudaErrorNotReady;
-  cudaError_t e = set_smem(op3::op3_kernel, op3::SMEM);
+  cudaError_t e = set_smem(op3::op3_kernel<double, 0>, op3::Lay<double>::SMEM);
   if (e != cudaSuccess) return e;
   if ((long long)gx * gy * gz == 0) return cudaSuccess;
   constexpr int TY = op3::TY;
   const dim3 grid((unsigned)gx, (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
-  op3::op3_kernel<<<grid, op3::NT, op3::SMEM, s>>>((const double*)x, (double*)y, (const double*)bm, gg, gx, gy,
-                                                  pair3_deltas(g, 0), dotp);
+  op3::op3_kernel<double, 0><<<grid, op3::NT, op3::Lay<double>::SMEM, s>>>(
+      (const double*)x, (double*)y, (const double*)bm, gg, gx, gy, pair3_deltas(g, 0), dotp, gg);
   return cudaGetLastError();
 }
 #endif
@@ -2424,6 +2424,35 @@ template <int D, typename T>
 cudaError_t launch_restrict(const void* x, const void* b, void* rc, const LevelGeom& gf, const LevelGeom& gc,
                             cudaStream_t s) {
   using C = Cfg<D, T>;
+#if !IPMG_DIRICHLET
+#ifndef IPMG_OP3_RESTRICT
+#define IPMG_OP3_RESTRICT 1   // 1: the residual + restriction through the staged operator (op3, MODE 1)
+#endif
+#ifndef IPMG_OP3_RESTRICT32_DEGREES
+#define IPMG_OP3_RESTRICT32_DEGREES 0x78   // fp32: k = 3..6 (tools/gpu_deg_restrict.sh: k = 2 3 % slower,
+                                           // k = 4 0.95 -> 0.71 ms); fp64: every op3 degree (all faster)
+#endif
+  if constexpr (D == 3) {
+    if (IPMG_OP3_RESTRICT && x != nullptr && op3_applies(gf) &&
+        (sizeof(T) == 8 || ((IPMG_OP3_RESTRICT32_DEGREES >> K) & 1)) && (reinterpret_cast<unsigned long long>(x) & 15) == 0 &&
+        (gf.ncells % (16 / (long long)sizeof(T))) == 0) {
+      LevelGeom gg = gf;
+      const int gx = gf.n[0] / 2, gy = gf.n[1] / 2;
+      int gz = slab_patches(gf, 2, 0);
+      gz = gz > 0 ? gz : 0;
+      gg.znb = gz;
+      gz = slab_sel_count(gz, gf.zsel);
+      if ((long long)gx * gy * gz == 0) return cudaSuccess;
+      cudaError_t e = set_smem(op3::op3_kernel<T, 1>, op3::Lay<T>::SMEM);
+      if (e != cudaSuccess) return e;
+      constexpr int TY = op3::TY;
+      const dim3 grid((unsigned)gx, (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
+      op3::op3_kernel<T, 1><<<grid, op3::NT, op3::Lay<T>::SMEM, s>>>((const T*)x, (T*)rc, (const T*)b, gg, gx, gy,
+                                                                    pair3_deltas(gf, 0), nullptr, gc);
+      return cudaGetLastError();
+    }
+  }
+#endif
   LevelGeom gg = gf;
   const dim3 grid = patch_grid<D, T>(gg, 0);
   if (grid.x * grid.y * grid.z == 0) return cudaSuccess;

@@ -46,6 +46,11 @@ def main():
     res["vmult64_ms"] = timeit(lambda: h.vmult(L, x64, y64))
     res["vmult32_ms"] = timeit(lambda: h.vmult(L, x32, o32))
     res["restrict32_ms"] = timeit(lambda: h.residual_restrict(L, x32, b32, rc))
+    h64 = ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=ipmg.FP64)
+    rc64 = torch.empty(nc, dtype=torch.float64, device="cuda")
+    b64 = x64 * 0.5
+    res["restrict64_ms"] = timeit(lambda: h64.residual_restrict(L, x64, b64, rc64))
+    h64.close()
     res["prolong32_ms"] = timeit(lambda: h.prolongate_add(L, rc, o32))
     hd = ipmg.Handle(dim, k, nl, coarse_cells=coarse, vcycle_precision=ipmg.FP32, kernel=ipmg.KERNEL_DIRICHLET)
     res["smooth_dir_c1_ms"] = timeit(lambda: hd.smooth_colour(L, x32, b32, o32, 1))
