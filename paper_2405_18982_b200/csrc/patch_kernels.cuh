@@ -2202,6 +2202,7 @@ inline bool op3_applies(const LevelGeom& g) {
 inline pair3::Deltas pair3_deltas(const LevelGeom& g, int colour);
 // the copies are widened to 16-byte granularity: x 16-byte aligned, and an even cell count
 // (the widened copy of the last cell ends inside the vector; ghost layers hold an even count)
+template <typename T>
 inline cudaError_t launch_op3(const void* x, void* y, const LevelGeom& g, const void* bm, double* dotp,
                               long long* nparts, cudaStream_t s) {
   LevelGeom gg = g;
@@ -2212,14 +2213,15 @@ inline cudaError_t launch_op3(const void* x, void* y, const LevelGeom& g, const 
   gz = slab_sel_count(gz, g.zsel);
   if (nparts) *nparts = (long long)gx * gy * gg.znb;   // full grid
   if (x == nullptr) return cudaSuccess;               // size query
-  if ((reinterpret_cast<unsigned long long>(x) & 15) != 0 || (g.ncells % 2) != 0) return cudaErrorNotReady;
-  cudaError_t e = set_smem(op3::op3_kernel<double, 0>, op3::Lay<double>::SMEM);
+  if ((reinterpret_cast<unsigned long long>(x) & 15) != 0 || (g.ncells % (16 / (long long)sizeof(T))) != 0)
+    return cudaErrorNotReady;
+  cudaError_t e = set_smem(op3::op3_kernel<T, 0>, op3::Lay<T>::SMEM);
   if (e != cudaSuccess) return e;
   if ((long long)gx * gy * gz == 0) return cudaSuccess;
   constexpr int TY = op3::TY;
   const dim3 grid((unsigned)gx, (unsigned)(TY * gz), (unsigned)((gy + TY - 1) / TY));
-  op3::op3_kernel<double, 0><<<grid, op3::NT, op3::Lay<double>::SMEM, s>>>(
-      (const double*)x, (double*)y, (const double*)bm, gg, gx, gy, pair3_deltas(g, 0), dotp, gg);
+  op3::op3_kernel<T, 0><<<grid, op3::NT, op3::Lay<T>::SMEM, s>>>((const T*)x, (T*)y, (const T*)bm, gg, gx, gy,
+                                                                pair3_deltas(g, 0), dotp, gg);
   return cudaGetLastError();
 }
 #endif
@@ -2229,9 +2231,14 @@ cudaError_t launch_vmult(const void* x, void* y, const LevelGeom& g, const void*
                          cudaStream_t s) {
   using C = Cfg<D, T>;
 #if !IPMG_DIRICHLET
-  if constexpr (D == 3 && sizeof(T) == 8) {
-    if (op3_applies(g)) {
-      const cudaError_t e = launch_op3(x, y, g, bm, dotp, nparts, s);
+#ifndef IPMG_OP3_VMULT32
+#define IPMG_OP3_VMULT32 0x70   // degrees whose fp32 operator also takes op3 (tools/gpu_deg_key.sh, C3 sizes:
+                                // k = 4 0.830 -> 0.711, k = 5 0.608 -> 0.561, k = 6 0.656 -> 0.586 ms;
+                                // k = 3 slower, 0.601 -> 0.642)
+#endif
+  if constexpr (D == 3) {
+    if (op3_applies(g) && (sizeof(T) == 8 || ((IPMG_OP3_VMULT32 >> K) & 1))) {
+      const cudaError_t e = launch_op3<T>(x, y, g, bm, dotp, nparts, s);
       if (e != cudaErrorNotReady) return e;
     }
   }
