@@ -73,7 +73,6 @@ __device__ __forceinline__ void trace_unit(T* F, const T* c, bool exists, int s,
   const int lc = ic % NC;
   T u[NC], du[NC];
   if (exists) {
-    const int jf = s == 0 ? NC - 1 : 0;   // face node: the neighbour's last node (low side), first (high)
     // element (normal j, point lb) of the 5x5 block at c + PS * lb + NS * j + TS * lc
     constexpr int PS = A == 0 ? NC : 1;            // point stride (t1 = y for A = 0, x otherwise)
     constexpr int NS = A == 0 ? 1 : (A == 1 ? NC : NC * NC);
@@ -90,9 +89,8 @@ __device__ __forceinline__ void trace_unit(T* F, const T* c, bool exists, int s,
 #pragma unroll
       for (int j = 0; j < NC; ++j) acc = fma_(s == 0 ? tb.d1[j] : tb.d0[j], v[lb][j], acc);
       du[lb] = acc;
-      u[lb] = s == 0 ? v[lb][NC - 1] : v[lb][0];
+      u[lb] = s == 0 ? v[lb][NC - 1] : v[lb][0];   // face node: the neighbour's last (low side) / first node
     }
-    (void)jf;
   } else {
 #pragma unroll
     for (int lb = 0; lb < NC; ++lb) u[lb] = du[lb] = T(0);
