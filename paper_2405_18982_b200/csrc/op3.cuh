@@ -129,6 +129,27 @@ __device__ __forceinline__ void t2_mass(T* F, int e) {
   store_lines<NP, 1>(base, 0, FROW, w);
 }
 
+#ifndef IPMG_OP3_T2HALF
+#define IPMG_OP3_T2HALF 1   // 1: the y mass of the z-normal family as half-line units on the idle threads
+#endif
+// one cell block (NC entries) of a t2_mass line: unit e of 8 NP = (side, kind, x index o, cell c)
+template <typename T>
+__device__ __forceinline__ void t2_mass_half(T* F, int e) {
+  const TabData<K, T>& tb = tab<T>();
+  const int c = e & 1, o = (e >> 1) % NP, sk = (e >> 1) / NP;
+  T* base = F + farr(2, sk >> 1, sk & 1) + o + FROW * NC * c;
+  T v[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) v[j] = base[FROW * j];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    T acc = T(0);
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc = fma_(tb.M[j][i], v[j], acc);
+    base[FROW * i] = acc;
+  }
+}
+
 // injection of face family a at tangential position pos into a line along a (operator sign +)
 template <typename T>
 __device__ __forceinline__ void inject(T (&y)[1][NP], const T* F, int a, int pos) {
@@ -171,6 +192,9 @@ __device__ __forceinline__ double op3_body(const T* __restrict__ x, T* __restric
                                            const LevelGeom& g, const PatchInfo& P, const pair3::Deltas& dl, T* X,
                                            T* T1, const T* OWN, T* F, bool dot) {
   using LY = Lay<T>;
+  // half-line units need idle threads; fp32 only (tools/gpu_deg_key.sh: fp32 restriction k = 4
+  // 0.711 -> 0.687 ms, k = 5, 6 -2 to -3 %; the fp64 operator 1 to 7 % slower with them)
+  constexpr bool HALF = IPMG_OP3_T2HALF && NT > NL && sizeof(T) == 4;
   const int t = threadIdx.x;
   // ---- x pass: T1 = M0 x, X = L0 x + x-normal family; the z-normal family's y mass on idle threads
   if (t < NL) {
@@ -194,11 +218,15 @@ __device__ __forceinline__ double op3_body(const T* __restrict__ x, T* __restric
     lap<FAST>(v, w, P.var[0]);
     inject(w, F, 0, i1 + FROW * i2);
     store_lines<NP, 1>(X + S1 * i1 + S2 * i2, 0, 1, w);
+  } else if (HALF) {
+    // the z-normal family's y mass as (line, cell) half-line units dealt over the threads
+    // without an x-line (k = 4: 80 units on 28 threads, at most 3 each)
+    for (int e = t - NL; e < 8 * NP; e += (HALF ? NT - NL : 1)) t2_mass_half(F, e);
   } else if (t - NL < 4 * NP) {
     t2_mass(F, t - NL);
   }
-  // lines the idle threads do not cover (k = 4: 40 lines, 28 idle threads) go to the first threads
-  if (NT - NL < 4 * NP && t < 4 * NP - (NT - NL)) t2_mass(F, NT - NL + t);
+  // (whole lines) the lines the idle threads do not cover go to the first threads
+  if (!HALF && NT - NL < 4 * NP && t < 4 * NP - (NT - NL)) t2_mass(F, NT - NL + t);
   __syncthreads();
   // ---- y pass: X = M1 X + L1 T1 + y-normal family, T1 = M1 T1
   const unsigned ly = __ldg(&pair3::g_lines[0][0][t]);
